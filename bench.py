@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark of the hypercube-convolution hot path (BASELINE.json metric).
+
+One "step" = one full convolution z = x * y of the named workload through the library's
+C ABI (hc_convolve / hc_convolve_sharded) with inputs resident in HBM.  Default workload
+(N = 1): BASELINE.json config 4, D = 20 fp64, x, y Exponential(1)-normalized (seeded,
+synthetic; hcgen).  With N > 1 GPUs (torchrun), the same D = 20 output is split into N
+contiguous ranges (zero-communication split by top trits, PAPER.md 166-177): total work
+fixed -> "scaling": "strong"; time = max over ranks.
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the oracle (Algorithm 1 in plain
+C, oracle/) on the host cores instead; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import hcgen  # noqa: E402
+
+METRIC = "output entries/s and achieved HBM GB/s vs roofline, D=20 fp64, 1/2/4/8 B200"
+UNIT = "output entries/s"
+
+WORKLOADS = {
+    "c4_d20_f64": dict(cfg="c4_d20_f64", D=20, desc="single pair D=20 fp64, Exp(1)-normalized (BASELINE config 4)"),
+    "c3_d16_i64": dict(cfg="c3_d16_i64", D=16, desc="single pair D=16 int64 uniform [0,2^16) (BASELINE config 3)"),
+    "c1_d10_i64": dict(cfg="c1_d10_i64", D=10, desc="single pair D=10 int64 uniform [0,9] (BASELINE config 1)"),
+    "c5_d22_f64": dict(cfg="c5_d22_f64", D=22, desc="single pair D=22 fp64 Exp(1)-normalized, sharded (BASELINE config 5)"),
+    "c2_b65536_d8_i64": dict(cfg="c2_b65536_d8_i64", D=8, B=65536,
+                             desc="65536 independent pairs D=8 int64 uniform [0,255] (BASELINE config 2)"),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload)
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=5)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        # under-load median: samples at >= 50% of max
+        mx = max(smax) if smax else None
+        loaded = [s for s in sm if mx and s >= 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_sample_rate(wl, budget_s=10.0, seed=99):
+    """Time the oracle (as it stands) on a bounded random sample of output cells of the
+    workload; returns (entries/s, cores, sample description, seconds)."""
+    import oracle
+    oracle.build()
+    w = WORKLOADS[wl]
+    D = w["D"]
+    cores = oracle.max_threads()
+    if "B" in w:
+        x, y = hcgen.config_inputs(w["cfg"])
+        rng = np.random.default_rng(seed)
+        nb = 256
+        bs = rng.choice(x.shape[0], size=nb, replace=False)
+        t0 = time.perf_counter()
+        oracle.conv_batched(x[bs], y[bs])
+        dt = time.perf_counter() - t0
+        n = nb * 3 ** D
+        return n / dt, cores, f"{nb} of {x.shape[0]} cubes, full Algorithm 1 each ({n} entries)", dt
+    x, y = hcgen.config_inputs(w["cfg"])
+    rng = np.random.default_rng(seed)
+    m = 3 ** D
+    n = 20000
+    total_n, total_t = 0, 0.0
+    while True:
+        ks = rng.integers(0, m, size=n, dtype=np.int64).astype(np.uint64)
+        t0 = time.perf_counter()
+        oracle.conv_cells(x, y, ks)
+        dt = time.perf_counter() - t0
+        total_n += n
+        total_t += dt
+        if total_t >= budget_s * 0.5 or n >= 1 << 26:
+            break
+        n = int(min(1 << 26, max(n * 2, n * (budget_s * 0.6 - total_t) / max(dt, 1e-3))))
+    return total_n / total_t, cores, (f"{total_n} uniformly random output cells of D={D} (Algorithm 1 gather "
+                                      f"form, avg (4/3)^{D} pairs per cell)"), total_t
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    wl = args.workload
+    rates = []
+    desc = None
+    cores = None
+    for _ in range(args.warmup):
+        oracle_sample_rate(wl, budget_s=1.0, seed=7)
+    t_all = 0.0
+    for s in range(args.steps):
+        r, cores, desc, dt = oracle_sample_rate(wl, budget_s=args.ref_budget, seed=100 + s)
+        rates.append(r)
+        t_all += dt
+    v = statistics.median(rates)
+    w = WORKLOADS[wl]
+    n_entries = (w.get("B", 1)) * 3 ** w["D"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * n_entries / v, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if "f64" in wl else "int64", "data": "synthetic",
+        "config": {"workload": wl, "desc": w["desc"], "D": w["D"], "output_entries": n_entries},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                         "cpu": cpu_model()},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "oracle = Algorithm 1 (PAPER.md 40-60) in plain C, OpenMP over cells; ms_per_step extrapolated "
+                "from the sampled rate to the whole output",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4_d20_f64", choices=sorted(WORKLOADS))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of oracle work per reference step")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import paper_1608_00206_b200.hc as hc
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    wl = args.workload
+    w = WORKLOADS[wl]
+    D = w["D"]
+    batched = "B" in w
+    x_np, y_np = hcgen.config_inputs(w["cfg"])
+    tdt = torch.float64 if x_np.dtype == np.float64 else torch.int64
+    xg = torch.from_numpy(x_np).cuda()
+    yg = torch.from_numpy(y_np).cuda()
+    stream = torch.cuda.current_stream()
+
+    if batched:
+        if world > 1:
+            raise SystemExit("batched workload is single-GPU in this bench")
+        B = w["B"]
+        z = torch.empty((B, 3 ** D), dtype=tdt, device="cuda")
+        n_local = B * 3 ** D
+        n_total = n_local
+
+        def step():
+            hc.convolve_batched(xg, yg, z)
+        in_bytes = 2 * B * 2 ** D * 8
+        prof_name = "tile"
+    else:
+        plan = hc.Plan(D, str(x_np.dtype), world, rank)
+        zb, ze = plan.shard_info()
+        z = torch.empty(ze - zb, dtype=tdt, device="cuda")
+        n_local = ze - zb
+        n_total = 3 ** D
+
+        def step():
+            plan.convolve_sharded(xg, yg, z)
+        in_bytes = 2 * 2 ** D * 8
+        prof_name = "tile"
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    hc.prof_reset()
+    hc.prof_enable(True)
+    l0 = hc.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = hc.launch_count() - l0
+    hc.prof_enable(False)
+    clocks = sampler.stop()
+    t_ms = e0.elapsed_time(e1)
+    ktime, kcount = hc.prof_read(prof_name)
+    hc.prof_reset()
+
+    t_max = t_ms
+    k_avg = ktime / max(kcount, 1)
+    if dist is not None:
+        tt = torch.tensor([t_ms, k_avg], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max, k_avg = float(tt[0]), float(tt[1])
+    ms_per_step = t_max / args.steps
+    value = n_total / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel: algorithmic bytes per launch / avg launch time
+    launches_per_step = kcount / max(args.steps, 1)
+    out_bytes_local = n_local * 8
+    in_bytes_local = in_bytes if not batched else in_bytes
+    alg_bytes_per_launch = (out_bytes_local + in_bytes_local * (1 if batched else 1)) / max(launches_per_step, 1)
+    peak, peak_src = load_peaks()
+    achieved = alg_bytes_per_launch / (k_avg / 1e3) / 1e9 if k_avg > 0 else None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": load_traffic(wl),
+                "kernel": prof_name, "alg_bytes_per_launch": alg_bytes_per_launch, "launch_ms": k_avg,
+                "peak_source": peak_src}
+
+    # end to end through the host-buffer C-ABI entry point (pinned host memory, copies inside)
+    e2e = None
+    if not args.no_e2e and not batched:
+        xh = torch.from_numpy(x_np).pin_memory()
+        yh = torch.from_numpy(y_np).pin_memory()
+        zh = torch.empty(n_local, dtype=tdt).pin_memory()
+        plan.convolve_host(xh, yh, zh)  # warm (allocates the plan's device workspace)
+        barrier()
+        ts = []
+        for _ in range(args.e2e_steps):
+            barrier()
+            t0 = time.perf_counter()
+            plan.convolve_host(xh, yh, zh)
+            ts.append(time.perf_counter() - t0)
+        tm = statistics.median(ts)
+        if dist is not None:
+            tt = torch.tensor([tm], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tm = float(tt[0])
+        e2e = {"value": n_total / tm, "unit": UNIT, "h2d_bytes_per_step": in_bytes,
+               "d2h_bytes_per_step": n_total * 8, "seconds_per_step": tm,
+               "path": "hc_convolve_host (pinned host x,y -> device -> pinned host z, chunked D2H overlapped)"}
+        del zh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r, cores, desc, dt = oracle_sample_rate(wl, budget_s=10.0)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc, "seconds": dt,
+               "cpu": cpu_model()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64" if tdt == torch.float64 else "int64",
+            "data": "synthetic",
+            "config": {"workload": wl, "desc": w["desc"], "D": D, "output_entries": n_total,
+                       "parallelism": f"output-split x{world}" if world > 1 else "single",
+                       "l2": "output (%.1f GB) > L2 (126 MB): every step streams the whole output" % (n_total * 8 / 1e9),
+                       "min_bytes_per_step": n_total * 8 + in_bytes},
+            "hbm_gbs_min_bytes": (n_total * 8 + in_bytes) / (ms_per_step / 1e3) / 1e9,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,118 @@
+/*
+ * hc.h -- C ABI of the B200-native hypercube-convolution library (libhc.so).
+ *
+ * Operation (Introduction):
+ *     z[k] = sum_{i,j : k = i + j} x[i] * y[j],   i, j in {0,1}^D,  k in {0,1,2}^D,
+ * computed with the paper's Karatsuba-style per-axis split (PAPER.md lines 185-192,
+ * Methods): forward (a0, a1) -> (a0, a0 + a1, a1), pointwise product, inverse
+ * (c0, c1, c2) -> (c0, (c1 - c0) - c2, c2) (the two subtraction loops of Algorithm 2,
+ * PAPER.md lines 248-251), combined with the paper's 4-sub-convolution split
+ * on the top axes.  The result is identical (int64) or equal
+ * up to rounding (fp64) to the naive Algorithm 1.
+ *
+ * Layout (all entry points):
+ *   x, y : 2^D elements, flat index i = sum_b i_b 2^b  (bit b = axis b; PAPER.md 109-112)
+ *   z    : 3^D elements, flat index k = sum_b k_b 3^b  (trit b = axis b)
+ *   batched: row-major [B][2^D] -> [B][3^D].
+ * Element types: HC_INT64 (computed as wrapping uint64: exact whenever the true z[k]
+ *   fits in int64; PAPER.md 191-192 "exact when the dynamic range allows (a+b)-a=b"),
+ *   HC_FP64 (IEEE double; deterministic, bit-identical run to run).
+ * Ownership: the caller owns x, y, z.  x and y are never modified (unlike Algorithm 2,
+ *   PAPER.md 225, which destroys its inputs).  z must not alias x or y.  A plan owns
+ *   only small tables, its own device buffers for the host-pointer entry point, and
+ *   counters.  Pointers must be 16-byte aligned (torch allocations are 256-B aligned).
+ * Streams: all device work is enqueued on `stream` (a cudaStream_t passed as void*;
+ *   NULL = legacy default stream).  Calls return after enqueueing; launch errors are
+ *   reported immediately (HC_ERR_CUDA); execution errors surface at the caller's sync.
+ * Errors: every function returns hc_status; nothing throws across the ABI.  D must be in
+ *   [1, HC_MAX_D] (D = 0 is rejected; the paper's recursion bottoms out at D = 1,
+ *   PAPER.md 255-263).
+ * Thread safety: plans are immutable after creation except for the host-buffer entry
+ *   point's workspace; do not call hc_convolve_host on one plan from two threads at once.
+ */
+#ifndef HC_H
+#define HC_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HC_MAX_D 24
+
+typedef enum {
+    HC_OK = 0,
+    HC_ERR_INVALID_DIM = 1,  /* D outside [1, HC_MAX_D], or B < 1 */
+    HC_ERR_DTYPE = 2,        /* unknown hc_dtype */
+    HC_ERR_NULL = 3,         /* a required pointer is NULL */
+    HC_ERR_ALIGN = 4,        /* a pointer is not 16-byte aligned */
+    HC_ERR_DEVICE = 5,       /* no CUDA device / wrong architecture (needs sm_100) */
+    HC_ERR_CAPACITY = 6,     /* device memory cannot hold the requested buffers */
+    HC_ERR_CUDA = 7,         /* a CUDA runtime call or kernel launch failed */
+    HC_ERR_SHARD = 9         /* rank / ngpu inconsistent with the plan */
+} hc_status;
+
+typedef enum { HC_INT64 = 0, HC_FP64 = 1 } hc_dtype;
+
+typedef struct hc_plan_s* hc_plan_t;
+
+/* Status text (static string). */
+const char* hc_status_str(hc_status s);
+
+/* 2^D and 3^D (0 if D is out of range). */
+uint64_t hc_in_len(int D);
+uint64_t hc_out_len(int D);
+
+/* Create a plan for one D-dimensional convolution on the current CUDA device.
+ * ngpu >= 1 ranks share the output: rank r owns the contiguous flat range of z returned
+ * by hc_shard_info (the zero-communication split of the output by its top trits, using
+ * the paper's 4-way split, PAPER.md 166-177).  ngpu == 1, rank == 0 for a single GPU. */
+hc_status hc_plan_create(hc_plan_t* out, int D, hc_dtype dtype, int ngpu, int rank);
+hc_status hc_plan_destroy(hc_plan_t plan);
+
+/* Flat range [z_begin, z_end) of z owned by `rank` under the plan's ngpu-way split. */
+hc_status hc_shard_info(hc_plan_t plan, int rank, uint64_t* z_begin, uint64_t* z_end);
+
+/* Pure host function (no device needed): the flat range [z_begin, z_end) of z that rank
+ * `rank` of `ngpu` owns for dimension D -- the same split hc_plan_create uses.  Ranges
+ * are contiguous, disjoint, cover [0, 3^D) in rank order, and are cut at output-slab
+ * boundaries so that the per-rank cost (one unit per direct-split pair plus a fixed cost
+ * per slab) is balanced. */
+hc_status hc_shard_range(int D, int ngpu, int rank, uint64_t* z_begin, uint64_t* z_end);
+
+/* Whole convolution: x, y device pointers (2^D elements), z device pointer (3^D). */
+hc_status hc_convolve(hc_plan_t plan, const void* x, const void* y, void* z, void* stream);
+
+/* This rank's share: x, y replicated (2^D each, device); z_shard has
+ * z_end - z_begin elements (device) and receives z[z_begin : z_end]. */
+hc_status hc_convolve_sharded(hc_plan_t plan, const void* x, const void* y, void* z_shard,
+                              void* stream);
+
+/* B independent convolutions of dimension D (row-major batches, device pointers). */
+hc_status hc_convolve_batched(int B, int D, hc_dtype dtype, const void* x, const void* y,
+                              void* z, void* stream);
+
+/* End-to-end entry point with HOST buffers: copies x, y (2^D each) to the device,
+ * computes this rank's share of z and copies it back into z_host (z_end - z_begin
+ * elements).  Host buffers should be pinned for full PCIe/C2C bandwidth.  Device
+ * output is produced and drained in chunks so the copy overlaps the computation.
+ * Synchronous: returns after z_host is complete. */
+hc_status hc_convolve_host(hc_plan_t plan, const void* x_host, const void* y_host,
+                           void* z_host, void* stream);
+
+/* Instrumentation (for bench.py / tests): cumulative number of kernels this library has
+ * launched in this process, and per-kernel device time when profiling is enabled
+ * (events recorded around each launch on the launching stream). */
+uint64_t hc_launch_count(void);
+void hc_prof_enable(int on);
+/* name: "small", "tile", "slab_p1", "slab_p2", "prep" ...; returns HC_OK and fills
+ * total milliseconds and launch count (0 if never launched).  Synchronizes the events. */
+hc_status hc_prof_read(const char* name, double* total_ms, uint64_t* launches);
+void hc_prof_reset(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HC_H */

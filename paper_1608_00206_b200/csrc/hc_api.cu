@@ -1,0 +1,355 @@
+// hc_api.cu -- the C ABI of include/hc.h: plans, dispatch, sharding, host entry point,
+// instrumentation.  See include/hc.h for the contract of every entry point.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/hc.h"
+#include "hc_common.cuh"
+#include "hc_tile.cuh"
+
+using namespace hc;
+
+// ---------------------------------------------------------------------------------------
+// instrumentation
+namespace {
+std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_prof{0};
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof_recs;
+
+struct LaunchScope {
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  LaunchScope(const char* n, cudaStream_t s) : name(n), st(s) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (g_prof.load(std::memory_order_relaxed)) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~LaunchScope() {
+    if (a) {
+      cudaEventRecord(b, st);
+      std::lock_guard<std::mutex> lk(g_prof_mu);
+      g_prof_recs.push_back({name, a, b});
+    }
+  }
+};
+}  // namespace
+
+extern "C" uint64_t hc_launch_count(void) { return g_launches.load(); }
+extern "C" void hc_prof_enable(int on) { g_prof.store(on ? 1 : 0); }
+extern "C" void hc_prof_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& r : g_prof_recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof_recs.clear();
+}
+extern "C" hc_status hc_prof_read(const char* name, double* total_ms, uint64_t* launches) {
+  if (!name || !total_ms || !launches) return HC_ERR_NULL;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  double t = 0;
+  uint64_t n = 0;
+  for (auto& r : g_prof_recs) {
+    if (r.name != name) continue;
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return HC_ERR_CUDA;
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) return HC_ERR_CUDA;
+    t += ms;
+    ++n;
+  }
+  *total_ms = t;
+  *launches = n;
+  return HC_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+extern "C" const char* hc_status_str(hc_status s) {
+  switch (s) {
+    case HC_OK: return "ok";
+    case HC_ERR_INVALID_DIM: return "invalid dimension (need 1 <= D <= HC_MAX_D, B >= 1)";
+    case HC_ERR_DTYPE: return "unknown dtype";
+    case HC_ERR_NULL: return "null pointer";
+    case HC_ERR_ALIGN: return "pointer not 16-byte aligned";
+    case HC_ERR_DEVICE: return "no usable CUDA device (needs sm_100)";
+    case HC_ERR_CAPACITY: return "insufficient device memory";
+    case HC_ERR_CUDA: return "CUDA error";
+    case HC_ERR_SHARD: return "rank/ngpu inconsistent with plan";
+  }
+  return "unknown status";
+}
+
+extern "C" uint64_t hc_in_len(int D) { return (D >= 1 && D <= HC_MAX_D) ? (1ull << D) : 0ull; }
+extern "C" uint64_t hc_out_len(int D) { return (D >= 1 && D <= HC_MAX_D) ? upow3(D) : 0ull; }
+
+namespace {
+
+constexpr int kTileL = 8;  // low axes handled inside one CTA (3^8 = 6561 outputs)
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+hc_status check_device() {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return HC_ERR_DEVICE; }
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) { cudaGetLastError(); return HC_ERR_DEVICE; }
+  if (p.major != 10) return HC_ERR_DEVICE;
+  return HC_OK;
+}
+
+// ---- launch of the tile engine for L = min(D, 8) --------------------------------------
+template <class T, int C, int B, int A>
+cudaError_t launch_tile_cfg(const T* x, const T* y, T* z, int D, uint64_t slab0, uint64_t nslab,
+                            uint64_t nitems, cudaStream_t st) {
+  using Cfg = TileCfg<T, C, B, A>;
+  auto kern = tile_kernel<T, C, B, A>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const uint64_t maxgrid = 0x7fffffffull;
+  for (uint64_t off = 0; off < nitems; off += maxgrid) {
+    const uint64_t n = nitems - off < maxgrid ? nitems - off : maxgrid;
+    // items [off, off+n): shift z and the slab origin; batches only appear with nslab = 3^k
+    LaunchScope ls("tile", st);
+    // when off > 0 the batch/slab split must be recomputed; offsets are multiples of nslab
+    // only for batched calls, so restrict chunking to whole batches or single-batch ranges
+    kern<<<(unsigned)n, Cfg::NT, Cfg::SMEM, st>>>(x, y, z + off * (uint64_t)Cfg::NOUT, D, slab0 + off, nslab);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+template <class T>
+cudaError_t launch_tile(const T* x, const T* y, T* z, int D, uint64_t slab0, uint64_t nslab,
+                        uint64_t nitems, cudaStream_t st) {
+  const int L = D < kTileL ? D : kTileL;
+  switch (L) {
+    case 1: return launch_tile_cfg<T, 1, 0, 0>(x, y, z, D, slab0, nslab, nitems, st);
+    case 2: return launch_tile_cfg<T, 2, 0, 0>(x, y, z, D, slab0, nslab, nitems, st);
+    case 3: return launch_tile_cfg<T, 3, 0, 0>(x, y, z, D, slab0, nslab, nitems, st);
+    case 4: return launch_tile_cfg<T, 3, 1, 0>(x, y, z, D, slab0, nslab, nitems, st);
+    case 5: return launch_tile_cfg<T, 3, 2, 0>(x, y, z, D, slab0, nslab, nitems, st);
+    case 6: return launch_tile_cfg<T, 3, 3, 0>(x, y, z, D, slab0, nslab, nitems, st);
+    case 7: return launch_tile_cfg<T, 3, 3, 1>(x, y, z, D, slab0, nslab, nitems, st);
+    default: return launch_tile_cfg<T, 3, 3, 2>(x, y, z, D, slab0, nslab, nitems, st);
+  }
+}
+
+cudaError_t launch_any(hc_dtype dt, const void* x, const void* y, void* z, int D, uint64_t slab0,
+                       uint64_t nslab, uint64_t nitems, cudaStream_t st) {
+  if (dt == HC_INT64)
+    return launch_tile<uint64_t>((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)z, D, slab0, nslab,
+                                 nitems, st);
+  return launch_tile<double>((const double*)x, (const double*)y, (double*)z, D, slab0, nslab, nitems, st);
+}
+
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+struct hc_plan_s {
+  int D;
+  hc_dtype dtype;
+  int ngpu, rank;
+  int L, k;                       // tile axes, top (direct-split) axes
+  uint64_t nslab;                 // 3^k output slabs of 3^L entries
+  std::vector<uint64_t> cuts;     // ngpu+1 slab boundaries (equal cost)
+  // host entry point workspace
+  void* dx = nullptr;
+  void* dy = nullptr;
+  void* dz[2] = {nullptr, nullptr};
+  uint64_t chunk_slabs = 0;
+  cudaStream_t hs[2] = {nullptr, nullptr};
+};
+
+// Equal-cost contiguous split of the 3^k output slabs over ngpu ranks.  Cost of slab
+// t_T ~ alpha + 2^{#1(t_T)}: one unit per direct-split pair (PAPER.md 166-177) plus alpha
+// for the slab's interpolation and store.
+static std::vector<uint64_t> compute_cuts(int k, int ngpu) {
+  const double alpha = 1.0;
+  const uint64_t n = upow3(k);
+  std::vector<double> pref(n + 1, 0.0);
+  for (uint64_t t = 0; t < n; ++t) {
+    uint64_t v = t;
+    int ones = 0;
+    for (int a = 0; a < k; ++a) {
+      if (v % 3 == 1) ++ones;
+      v /= 3;
+    }
+    pref[t + 1] = pref[t] + alpha + (double)(1ull << ones);
+  }
+  std::vector<uint64_t> cuts(ngpu + 1, 0);
+  cuts[ngpu] = n;
+  uint64_t j = 0;
+  for (int r = 1; r < ngpu; ++r) {
+    const double target = pref[n] * r / ngpu;
+    while (j < n && pref[j] < target) ++j;
+    // nearest boundary to the target, then keep every rank non-empty
+    uint64_t c = (j > 0 && target - pref[j - 1] < pref[j] - target) ? j - 1 : j;
+    const uint64_t lo = cuts[r - 1] + 1, hi = n - (uint64_t)(ngpu - r);
+    c = c < lo ? lo : (c > hi ? hi : c);
+    cuts[r] = c;
+  }
+  return cuts;
+}
+
+static inline int tile_axes(int D) { return D < kTileL ? D : kTileL; }
+
+extern "C" hc_status hc_shard_range(int D, int ngpu, int rank, uint64_t* zb, uint64_t* ze) {
+  if (!zb || !ze) return HC_ERR_NULL;
+  if (D < 1 || D > HC_MAX_D) return HC_ERR_INVALID_DIM;
+  const int L = tile_axes(D), k = D - L;
+  if (ngpu < 1 || rank < 0 || rank >= ngpu || (uint64_t)ngpu > upow3(k)) return HC_ERR_SHARD;
+  std::vector<uint64_t> cuts = compute_cuts(k, ngpu);
+  *zb = cuts[rank] * upow3(L);
+  *ze = cuts[rank + 1] * upow3(L);
+  return HC_OK;
+}
+
+extern "C" hc_status hc_plan_create(hc_plan_t* out, int D, hc_dtype dtype, int ngpu, int rank) {
+  if (!out) return HC_ERR_NULL;
+  *out = nullptr;
+  if (D < 1 || D > HC_MAX_D) return HC_ERR_INVALID_DIM;
+  if (dtype != HC_INT64 && dtype != HC_FP64) return HC_ERR_DTYPE;
+  if (ngpu < 1 || rank < 0 || rank >= ngpu) return HC_ERR_SHARD;
+  hc_status ds = check_device();
+  if (ds != HC_OK) return ds;
+  auto* p = new hc_plan_s();
+  p->D = D;
+  p->dtype = dtype;
+  p->ngpu = ngpu;
+  p->rank = rank;
+  p->L = tile_axes(D);
+  p->k = D - p->L;
+  p->nslab = upow3(p->k);
+  if ((uint64_t)ngpu > p->nslab) {
+    delete p;
+    return HC_ERR_SHARD;
+  }
+  p->cuts = compute_cuts(p->k, ngpu);
+  *out = p;
+  return HC_OK;
+}
+
+extern "C" hc_status hc_plan_destroy(hc_plan_t p) {
+  if (!p) return HC_ERR_NULL;
+  cudaFree(p->dx);
+  cudaFree(p->dy);
+  cudaFree(p->dz[0]);
+  cudaFree(p->dz[1]);
+  for (auto& s : p->hs)
+    if (s) cudaStreamDestroy(s);
+  delete p;
+  return HC_OK;
+}
+
+extern "C" hc_status hc_shard_info(hc_plan_t p, int rank, uint64_t* zb, uint64_t* ze) {
+  if (!p || !zb || !ze) return HC_ERR_NULL;
+  if (rank < 0 || rank >= p->ngpu) return HC_ERR_SHARD;
+  const uint64_t tile = upow3(p->L);
+  *zb = p->cuts[rank] * tile;
+  *ze = p->cuts[rank + 1] * tile;
+  return HC_OK;
+}
+
+static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, uint64_t s0, uint64_t s1,
+                           cudaStream_t st) {
+  if (s1 <= s0) return HC_OK;
+  cudaError_t e = launch_any(p->dtype, x, y, z, p->D, s0, p->nslab, s1 - s0, st);
+  return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
+}
+
+extern "C" hc_status hc_convolve(hc_plan_t p, const void* x, const void* y, void* z, void* stream) {
+  if (!p || !x || !y || !z) return HC_ERR_NULL;
+  if (!aligned16(x) || !aligned16(y) || !aligned16(z)) return HC_ERR_ALIGN;
+  return run_range(p, x, y, z, 0, p->nslab, (cudaStream_t)stream);
+}
+
+extern "C" hc_status hc_convolve_sharded(hc_plan_t p, const void* x, const void* y, void* zs, void* stream) {
+  if (!p || !x || !y || !zs) return HC_ERR_NULL;
+  if (!aligned16(x) || !aligned16(y) || !aligned16(zs)) return HC_ERR_ALIGN;
+  return run_range(p, x, y, zs, p->cuts[p->rank], p->cuts[p->rank + 1], (cudaStream_t)stream);
+}
+
+extern "C" hc_status hc_convolve_batched(int B, int D, hc_dtype dtype, const void* x, const void* y, void* z,
+                                         void* stream) {
+  if (B < 1 || D < 1 || D > HC_MAX_D) return HC_ERR_INVALID_DIM;
+  if (dtype != HC_INT64 && dtype != HC_FP64) return HC_ERR_DTYPE;
+  if (!x || !y || !z) return HC_ERR_NULL;
+  if (!aligned16(x) || !aligned16(y) || !aligned16(z)) return HC_ERR_ALIGN;
+  hc_status ds = check_device();
+  if (ds != HC_OK) return ds;
+  const int L = tile_axes(D);
+  const uint64_t nslab = upow3(D - L);
+  const uint64_t nitems = (uint64_t)B * nslab;
+  if (nitems > 0x7fffffffull) return HC_ERR_INVALID_DIM;
+  cudaError_t e = launch_any(dtype, x, y, z, D, 0, nslab, nitems, (cudaStream_t)stream);
+  return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
+}
+
+extern "C" hc_status hc_convolve_host(hc_plan_t p, const void* xh, const void* yh, void* zh, void* stream) {
+  if (!p || !xh || !yh || !zh) return HC_ERR_NULL;
+  const size_t esz = 8;
+  const uint64_t nin = 1ull << p->D;
+  const uint64_t tile = upow3(p->L);
+  const uint64_t s0 = p->cuts[p->rank], s1 = p->cuts[p->rank + 1];
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!p->dx) {
+    if (cudaMalloc(&p->dx, nin * esz) != cudaSuccess || cudaMalloc(&p->dy, nin * esz) != cudaSuccess) {
+      cudaGetLastError();
+      return HC_ERR_CAPACITY;
+    }
+    // chunks of ~1 GiB of output, double-buffered so D2H of chunk c overlaps chunk c+1
+    uint64_t cs = ((1ull << 30) / esz) / tile;
+    if (cs < 1) cs = 1;
+    if (cs > s1 - s0) cs = s1 - s0;
+    if (cs < 1) cs = 1;
+    p->chunk_slabs = cs;
+    for (int i = 0; i < 2; ++i) {
+      if (cudaMalloc(&p->dz[i], cs * tile * esz) != cudaSuccess) {
+        cudaGetLastError();
+        return HC_ERR_CAPACITY;
+      }
+      if (cudaStreamCreateWithFlags(&p->hs[i], cudaStreamNonBlocking) != cudaSuccess) return HC_ERR_CUDA;
+    }
+  }
+  if (cudaMemcpyAsync(p->dx, xh, nin * esz, cudaMemcpyHostToDevice, st) != cudaSuccess) return HC_ERR_CUDA;
+  if (cudaMemcpyAsync(p->dy, yh, nin * esz, cudaMemcpyHostToDevice, st) != cudaSuccess) return HC_ERR_CUDA;
+  cudaEvent_t ready;
+  cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  cudaEventRecord(ready, st);
+  int i = 0;
+  for (uint64_t c = s0; c < s1; c += p->chunk_slabs, i ^= 1) {
+    const uint64_t ce = c + p->chunk_slabs < s1 ? c + p->chunk_slabs : s1;
+    cudaStream_t hs = p->hs[i];
+    cudaStreamWaitEvent(hs, ready, 0);
+    hc_status r = run_range(p, p->dx, p->dy, p->dz[i], c, ce, hs);
+    if (r != HC_OK) return r;
+    if (cudaMemcpyAsync((char*)zh + (c - s0) * tile * esz, p->dz[i], (ce - c) * tile * esz,
+                        cudaMemcpyDeviceToHost, hs) != cudaSuccess)
+      return HC_ERR_CUDA;
+  }
+  cudaError_t e1 = cudaStreamSynchronize(p->hs[0]);
+  cudaError_t e2 = cudaStreamSynchronize(p->hs[1]);
+  cudaEventDestroy(ready);
+  return (e1 == cudaSuccess && e2 == cudaSuccess) ? HC_OK : HC_ERR_CUDA;
+}

@@ -1,0 +1,203 @@
+"""Thin ctypes binding over libhc.so (include/hc.h).  Argument marshalling only: every step
+of the convolution runs in the CUDA kernels behind the C ABI.  torch supplies device
+memory and streams; nothing here computes on the host, and there is no fallback: a
+missing or unloadable libhc.so raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhc.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "hc.h")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libhc.so not built at {LIB_PATH}; run `python -m paper_1608_00206_b200.build` "
+                      "(there is no CPU fallback)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+HC_INT64, HC_FP64 = 0, 1
+STATUS = {0: "HC_OK", 1: "HC_ERR_INVALID_DIM", 2: "HC_ERR_DTYPE", 3: "HC_ERR_NULL", 4: "HC_ERR_ALIGN",
+          5: "HC_ERR_DEVICE", 6: "HC_ERR_CAPACITY", 7: "HC_ERR_CUDA", 9: "HC_ERR_SHARD"}
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_U64 = ctypes.c_uint64
+_lib.hc_status_str.argtypes = [_I]
+_lib.hc_status_str.restype = ctypes.c_char_p
+_lib.hc_in_len.argtypes = [_I]
+_lib.hc_in_len.restype = _U64
+_lib.hc_out_len.argtypes = [_I]
+_lib.hc_out_len.restype = _U64
+_lib.hc_plan_create.argtypes = [ctypes.POINTER(_P), _I, _I, _I, _I]
+_lib.hc_plan_destroy.argtypes = [_P]
+_lib.hc_shard_info.argtypes = [_P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64)]
+_lib.hc_shard_range.argtypes = [_I, _I, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64)]
+_lib.hc_convolve.argtypes = [_P, _P, _P, _P, _P]
+_lib.hc_convolve_sharded.argtypes = [_P, _P, _P, _P, _P]
+_lib.hc_convolve_batched.argtypes = [_I, _I, _I, _P, _P, _P, _P]
+_lib.hc_convolve_host.argtypes = [_P, _P, _P, _P, _P]
+_lib.hc_launch_count.restype = _U64
+_lib.hc_prof_enable.argtypes = [_I]
+_lib.hc_prof_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_U64)]
+
+
+class HCError(RuntimeError):
+    def __init__(self, code: int, where: str = ""):
+        self.code = code
+        super().__init__(f"{where}: {STATUS.get(code, code)} ({_lib.hc_status_str(code).decode()})")
+
+
+def _ok(code: int, where: str):
+    if code != 0:
+        raise HCError(code, where)
+
+
+def exported_symbols():
+    """Names declared in include/hc.h (the test suite checks libhc.so exports each)."""
+    with open(HEADER) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(hc_[a-z0-9_]+)\s*\(", text)))
+
+
+def in_len(D: int) -> int:
+    return int(_lib.hc_in_len(D))
+
+
+def out_len(D: int) -> int:
+    return int(_lib.hc_out_len(D))
+
+
+def shard_range(D: int, ngpu: int, rank: int):
+    """Host-only: [z_begin, z_end) owned by `rank` of `ngpu` (hc_shard_range)."""
+    b, e = _U64(), _U64()
+    _ok(_lib.hc_shard_range(D, ngpu, rank, ctypes.byref(b), ctypes.byref(e)), "hc_shard_range")
+    return int(b.value), int(e.value)
+
+
+def _dtype_code(dtype) -> int:
+    s = str(dtype)
+    if s.endswith("int64"):
+        return HC_INT64
+    if s.endswith("float64"):
+        return HC_FP64
+    raise TypeError(f"hypercube convolution supports int64 and float64, got {dtype}")
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _dev(t, n, dtype_code, name):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.numel() != n:
+        raise ValueError(f"{name} must have {n} elements, got {t.numel()}")
+    if _dtype_code(t.dtype) != dtype_code:
+        raise TypeError(f"{name} dtype {t.dtype} does not match the plan")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Plan:
+    """hc_plan_create(D, dtype, ngpu, rank)."""
+
+    def __init__(self, D: int, dtype="float64", ngpu: int = 1, rank: int = 0):
+        self.D, self.ngpu, self.rank = D, ngpu, rank
+        self.dtype_code = _dtype_code(dtype)
+        h = _P()
+        _ok(_lib.hc_plan_create(ctypes.byref(h), D, self.dtype_code, ngpu, rank), "hc_plan_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.hc_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def shard_info(self, rank=None):
+        b, e = _U64(), _U64()
+        _ok(_lib.hc_shard_info(self._h, self.rank if rank is None else rank, ctypes.byref(b), ctypes.byref(e)),
+            "hc_shard_info")
+        return int(b.value), int(e.value)
+
+    def convolve(self, x, y, z, stream=None):
+        n, m = in_len(self.D), out_len(self.D)
+        _ok(_lib.hc_convolve(self._h, _dev(x, n, self.dtype_code, "x"), _dev(y, n, self.dtype_code, "y"),
+                             _dev(z, m, self.dtype_code, "z"), _P(_stream_ptr(stream))), "hc_convolve")
+        return z
+
+    def convolve_sharded(self, x, y, z_shard, stream=None):
+        n = in_len(self.D)
+        b, e = self.shard_info()
+        _ok(_lib.hc_convolve_sharded(self._h, _dev(x, n, self.dtype_code, "x"), _dev(y, n, self.dtype_code, "y"),
+                                     _dev(z_shard, e - b, self.dtype_code, "z_shard"), _P(_stream_ptr(stream))),
+            "hc_convolve_sharded")
+        return z_shard
+
+    def convolve_host(self, x_host, y_host, z_host, stream=None):
+        """Host (CPU, ideally pinned) tensors; copies in, computes, copies this rank's share out."""
+        n = in_len(self.D)
+        b, e = self.shard_info()
+        for t, want, name in ((x_host, n, "x"), (y_host, n, "y"), (z_host, e - b, "z")):
+            if t.is_cuda or not t.is_contiguous() or t.numel() != want or _dtype_code(t.dtype) != self.dtype_code:
+                raise ValueError(f"{name}: need a contiguous host tensor of {want} {self.dtype_code} elements")
+        _ok(_lib.hc_convolve_host(self._h, _P(x_host.data_ptr()), _P(y_host.data_ptr()), _P(z_host.data_ptr()),
+                                  _P(_stream_ptr(stream))), "hc_convolve_host")
+        return z_host
+
+
+def convolve_batched(x, y, z, stream=None):
+    """x, y: [B, 2^D] CUDA tensors; z: [B, 3^D]."""
+    if x.dim() != 2 or x.shape != y.shape:
+        raise ValueError("x, y must be [B, 2^D]")
+    B, n = x.shape
+    D = n.bit_length() - 1
+    if (1 << D) != n:
+        raise ValueError("row length must be 2^D")
+    code = _dtype_code(x.dtype)
+    _ok(_lib.hc_convolve_batched(B, D, code, _dev(x, B * n, code, "x"), _dev(y, B * n, code, "y"),
+                                 _dev(z, B * out_len(D), code, "z"), _P(_stream_ptr(stream))),
+        "hc_convolve_batched")
+    return z
+
+
+def convolve(x, y, z=None, stream=None):
+    """One-shot convenience: plan + hc_convolve on CUDA tensors x, y (2^D each)."""
+    import torch
+    n = x.numel()
+    D = n.bit_length() - 1
+    if z is None:
+        z = torch.empty(3 ** D, dtype=x.dtype, device=x.device)
+    Plan(D, x.dtype).convolve(x, y, z, stream)
+    return z
+
+
+def launch_count() -> int:
+    return int(_lib.hc_launch_count())
+
+
+def prof_enable(on: bool = True):
+    _lib.hc_prof_enable(1 if on else 0)
+
+
+def prof_reset():
+    _lib.hc_prof_reset()
+
+
+def prof_read(name: str):
+    ms = ctypes.c_double()
+    n = _U64()
+    _ok(_lib.hc_prof_read(name.encode(), ctypes.byref(ms), ctypes.byref(n)), "hc_prof_read")
+    return float(ms.value), int(n.value)

@@ -1,0 +1,199 @@
+"""Parity of the CUDA path (through the C ABI) against the oracle (Algorithm 1, PAPER.md 40-60).
+
+int64: bit-exact at every compared cell.  fp64: max|z_gpu - z_oracle| <= 1e-12 * sum|x| *
+sum|y| (BASELINE.json north_star tolerance).  Sizes span several tiles and
+ragged tails; BASELINE.json's full sizes are checked in full where the oracle can finish
+in seconds (C1, C2, C3) and on sampled cells plus whole-output invariants otherwise (C4).
+"""
+import numpy as np
+import pytest
+
+import hcgen
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def hc():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1608_00206_b200.hc as hcmod
+    return hcmod
+
+
+def _gpu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _run(hc, x, y):
+    D = x.shape[0].bit_length() - 1
+    z = torch.empty(3 ** D, dtype=torch.float64 if x.dtype == np.float64 else torch.int64, device="cuda")
+    hc.Plan(D, str(x.dtype)).convolve(_gpu(x), _gpu(y), z)
+    torch.cuda.synchronize()
+    return z
+
+
+def _assert_close(got, want, x, y):
+    if want.dtype == np.int64:
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, f"{bad.size} int64 cells differ, first at {bad[:5]}: {got[bad[:5]]} vs {want[bad[:5]]}"
+    else:
+        scale = float(np.abs(x).sum() * np.abs(y).sum())
+        err = float(np.max(np.abs(got - want))) if got.size else 0.0
+        assert err <= TOL * scale, f"max err {err:.3e} > {TOL} * {scale:.3e}"
+
+
+@pytest.mark.parametrize("dtype", ["int64", "float64"])
+@pytest.mark.parametrize("D", list(range(1, 13)))
+def test_single_pair_all_D(hc, orc, D, dtype):
+    for seed in (1, 2):
+        if dtype == "int64":
+            x, y = hcgen.make_pair(D, "int64", "uniform", 100 * D + seed, -1000, 1000)
+        else:
+            x, y = hcgen.make_pair(D, "float64", "exp_norm", 100 * D + seed)
+        got = _run(hc, x, y).cpu().numpy()
+        _assert_close(got, orc.conv(x, y), x, y)
+
+
+@pytest.mark.parametrize("D", [1, 2, 3, 5, 7, 8, 9, 10])
+def test_batched_small(hc, orc, D):
+    B = 7
+    xb, yb = hcgen.make_batched_fast(B, D, 0, 255, 31 + D)
+    z = torch.empty((B, 3 ** D), dtype=torch.int64, device="cuda")
+    hc.convolve_batched(_gpu(xb), _gpu(yb), z)
+    torch.cuda.synchronize()
+    assert np.array_equal(z.cpu().numpy(), orc.conv_batched(xb, yb))
+    xf = (xb.astype(np.float64) + 0.25) / 256.0
+    yf = (yb.astype(np.float64) + 0.5) / 256.0
+    zf = torch.empty((B, 3 ** D), dtype=torch.float64, device="cuda")
+    hc.convolve_batched(_gpu(xf), _gpu(yf), zf)
+    torch.cuda.synchronize()
+    want = orc.conv_batched(xf, yf)
+    for b in range(B):
+        _assert_close(zf[b].cpu().numpy(), want[b], xf[b], yf[b])
+
+
+def test_config_c1_d10_int64(hc, orc):
+    x, y = hcgen.config_inputs("c1_d10_i64")
+    got = _run(hc, x, y).cpu().numpy()
+    assert np.array_equal(got, orc.conv(x, y))
+
+
+def test_config_c2_batched_d8_full(hc, orc):
+    # BASELINE.json config 2 at full size, every cell of every cube
+    x, y = hcgen.config_inputs("c2_b65536_d8_i64")
+    B = x.shape[0]
+    z = torch.empty((B, 3 ** 8), dtype=torch.int64, device="cuda")
+    hc.convolve_batched(_gpu(x), _gpu(y), z)
+    torch.cuda.synchronize()
+    assert np.array_equal(z.cpu().numpy(), orc.conv_batched(x, y))
+
+
+def test_config_c3_d16_int64_full(hc, orc):
+    x, y = hcgen.config_inputs("c3_d16_i64")
+    got = _run(hc, x, y).cpu().numpy()
+    assert np.array_equal(got, orc.conv(x, y))
+
+
+def test_d16_all_ones_and_separable(hc):
+    D = 16
+    x, y = hcgen.all_ones(D)
+    got = _run(hc, x, y).cpu().numpy()
+    # closed form z[k] = 2^{#trits(k) == 1}
+    ones = np.zeros(1, dtype=np.int64)
+    for _ in range(D):
+        ones = np.concatenate([ones, ones + 1, ones])
+    assert np.array_equal(got, (1 << ones).astype(np.int64))
+    fx, fy = hcgen.separable_factors(D, seed=1103, lo=1, hi=2)
+    x = hcgen.tensor_product(fx)
+    y = hcgen.tensor_product(fy)
+    want = np.ones(1, dtype=np.int64)
+    for b in range(D):
+        c = np.array([fx[b, 0] * fy[b, 0], fx[b, 0] * fy[b, 1] + fx[b, 1] * fy[b, 0], fx[b, 1] * fy[b, 1]])
+        want = np.concatenate([want * c[0], want * c[1], want * c[2]])
+    assert np.array_equal(_run(hc, x, y).cpu().numpy(), want)
+
+
+def _sample_cells(D, n, seed):
+    m = 3 ** D
+    rng = np.random.default_rng(seed)
+    ks = rng.integers(0, m, size=n, dtype=np.int64)
+    # plus whole contiguous blocks: the first tiles, a ragged tail, and the all-ones-trit region
+    ones_idx = sum(3 ** b for b in range(D))
+    blocks = [np.arange(0, 3 ** 9), np.arange(m - 3 ** 8 - 17, m),
+              np.arange(max(0, ones_idx - 3 ** 8), min(m, ones_idx + 3 ** 8))]
+    return np.unique(np.concatenate([ks] + blocks)).astype(np.int64)
+
+
+@pytest.mark.slow
+def test_config_c4_d20_fp64_sampled(hc, orc):
+    x, y = hcgen.config_inputs("c4_d20_f64")
+    D = 20
+    z = _run(hc, x, y)
+    ks = _sample_cells(D, 20000, 4)
+    got = z[torch.from_numpy(ks).cuda()].cpu().numpy()
+    want = orc.conv_cells(x, y, ks.astype(np.uint64))
+    _assert_close(got, want, x, y)
+    # whole-output invariant: mass conservation sum z = sum x * sum y
+    tot = float(z.sum().item())
+    assert abs(tot - float(x.sum()) * float(y.sum())) <= 1e-9
+    # determinism: a second run is bit-identical
+    z2 = _run(hc, x, y)
+    assert torch.equal(z, z2)
+
+
+@pytest.mark.parametrize("ngpu", [2, 3, 8])
+def test_sharded_concat_equals_full(hc, ngpu):
+    D = 12
+    x, y = hcgen.make_pair(D, "int64", "uniform", 55, 0, 1 << 16)
+    full = _run(hc, x, y)
+    xs, ys = _gpu(x), _gpu(y)
+    parts = []
+    prev = 0
+    for r in range(ngpu):
+        p = hc.Plan(D, "int64", ngpu, r)
+        b, e = p.shard_info()
+        assert b == prev and (b, e) == hc.shard_range(D, ngpu, r)
+        prev = e
+        zs = torch.empty(e - b, dtype=torch.int64, device="cuda")
+        p.convolve_sharded(xs, ys, zs)
+        parts.append(zs)
+    assert prev == 3 ** D
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts), full)
+
+
+def test_host_entry_point(hc, orc):
+    D = 13
+    x, y = hcgen.make_pair(D, "float64", "exp_norm", 77)
+    p = hc.Plan(D, "float64")
+    zh = torch.empty(3 ** D, dtype=torch.float64).pin_memory()
+    p.convolve_host(torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory(), zh)
+    zd = _run(hc, x, y).cpu()
+    assert torch.equal(zh, zd)
+    _assert_close(zh.numpy(), orc.conv(x, y), x, y)
+
+
+def test_commutativity_int64(hc):
+    D = 11
+    x, y = hcgen.make_pair(D, "int64", "uniform", 9, -5000, 5000)
+    assert torch.equal(_run(hc, x, y), _run(hc, y, x))
+
+
+def test_errors(hc):
+    with pytest.raises(hc.HCError):
+        hc.Plan(0)
+    with pytest.raises(hc.HCError):
+        hc.Plan(hc.in_len(1) * 0 + 25)
+    p = hc.Plan(4, "int64")
+    x = torch.zeros(16, dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError):
+        p.convolve(x, x, torch.empty(80, dtype=torch.int64, device="cuda"))
+    # misaligned device pointer -> HC_ERR_ALIGN
+    buf = torch.zeros(100, dtype=torch.int64, device="cuda")
+    with pytest.raises(hc.HCError) as ei:
+        p.convolve(buf[1:17], buf[1:17], torch.empty(81, dtype=torch.int64, device="cuda"))
+    assert ei.value.code == 4
