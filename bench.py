@@ -113,6 +113,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+def reduce_max(vals, dist=None, device="cuda"):
+    """Elementwise max over ranks (device time is reported as the slowest rank's)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return list(vals)
+    import torch
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -286,14 +296,12 @@ def main():
     clocks = sampler.stop()
     t_ms = e0.elapsed_time(e1)
     ktime, kcount = hc.prof_read(prof_name)
+    if kcount == 0:
+        prof_name = "slab"
+        ktime, kcount = hc.prof_read(prof_name)
     hc.prof_reset()
 
-    t_max = t_ms
-    k_avg = ktime / max(kcount, 1)
-    if dist is not None:
-        tt = torch.tensor([t_ms, k_avg], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max, k_avg = float(tt[0]), float(tt[1])
+    t_max, k_avg = reduce_max([t_ms, ktime / max(kcount, 1)], dist)
     ms_per_step = t_max / args.steps
     value = n_total / (ms_per_step / 1e3)
 
@@ -323,11 +331,7 @@ def main():
             t0 = time.perf_counter()
             plan.convolve_host(xh, yh, zh)
             ts.append(time.perf_counter() - t0)
-        tm = statistics.median(ts)
-        if dist is not None:
-            tt = torch.tensor([tm], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            tm = float(tt[0])
+        tm = reduce_max([statistics.median(ts)], dist)[0]
         e2e = {"value": n_total / tm, "unit": UNIT, "h2d_bytes_per_step": in_bytes,
                "d2h_bytes_per_step": n_total * 8, "seconds_per_step": tm,
                "path": "hc_convolve_host (pinned host x,y -> device -> pinned host z, chunked D2H overlapped)"}

@@ -103,13 +103,23 @@ constexpr int kTileL = 8;  // low axes handled inside one CTA (3^8 = 6561 output
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Device capability check, cached per device (cudaGetDeviceProperties is slow).
 hc_status check_device() {
+  static std::atomic<int> ok_dev[64];  // 0 = unknown, 1 = ok, 2 = unusable
   int dev = -1;
-  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return HC_ERR_DEVICE; }
-  cudaDeviceProp p;
-  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) { cudaGetLastError(); return HC_ERR_DEVICE; }
-  if (p.major != 10) return HC_ERR_DEVICE;
-  return HC_OK;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) { cudaGetLastError(); return HC_ERR_DEVICE; }
+  if (dev < 64) {
+    const int v = ok_dev[dev].load(std::memory_order_relaxed);
+    if (v) return v == 1 ? HC_OK : HC_ERR_DEVICE;
+  }
+  int major = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return HC_ERR_DEVICE;
+  }
+  const bool ok = major == 10;
+  if (dev < 64) ok_dev[dev].store(ok ? 1 : 2, std::memory_order_relaxed);
+  return ok ? HC_OK : HC_ERR_DEVICE;
 }
 
 // ---- launch of the tile engine for L = min(D, 8) --------------------------------------
@@ -143,9 +153,9 @@ cudaError_t launch_tile(const T* x, const T* y, T* z, int D, uint64_t slab0, uin
                         uint64_t nitems, cudaStream_t st) {
   const int L = D < kTileL ? D : kTileL;
   switch (L) {
-    case 1: return launch_tile_cfg<T, 1, 0, 0>(x, y, z, D, slab0, nslab, nitems, st);
-    case 2: return launch_tile_cfg<T, 2, 0, 0>(x, y, z, D, slab0, nslab, nitems, st);
-    case 3: return launch_tile_cfg<T, 3, 0, 0>(x, y, z, D, slab0, nslab, nitems, st);
+    case 1: return launch_tile_cfg<T, 0, 1, 0>(x, y, z, D, slab0, nslab, nitems, st);
+    case 2: return launch_tile_cfg<T, 1, 1, 0>(x, y, z, D, slab0, nslab, nitems, st);
+    case 3: return launch_tile_cfg<T, 2, 1, 0>(x, y, z, D, slab0, nslab, nitems, st);
     case 4: return launch_tile_cfg<T, 3, 1, 0>(x, y, z, D, slab0, nslab, nitems, st);
     case 5: return launch_tile_cfg<T, 3, 2, 0>(x, y, z, D, slab0, nslab, nitems, st);
     case 6: return launch_tile_cfg<T, 3, 3, 0>(x, y, z, D, slab0, nslab, nitems, st);
@@ -162,22 +172,80 @@ cudaError_t launch_any(hc_dtype dt, const void* x, const void* y, void* z, int D
   return launch_tile<double>((const double*)x, (const double*)y, (double*)z, D, slab0, nslab, nitems, st);
 }
 
+// ---- launch of the two-level slab engine -----------------------------------------------
+template <class T, int M>
+cudaError_t launch_slab_m(const T* x, const T* y, T* z, int k, uint64_t slab0, uint32_t nslab, uint32_t* ctr,
+                          cudaStream_t st) {
+  using Cfg = TileCfg<T, 3, 3, 2>;
+  auto kern = slab_kernel<T, 3, 3, 2, M>;
+  static int grid_max = 0;
+  if (!grid_max) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    int occ = 0, dev = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NT, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    grid_max = occ * sms;
+  }
+  const uint64_t items = (uint64_t)nslab * (upow3(M) + upow3(Cfg::L) / P2W);
+  const unsigned grid = (unsigned)(items < (uint64_t)grid_max ? items : (uint64_t)grid_max);
+  cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * (1 + (size_t)nslab), st);
+  if (e != cudaSuccess) return e;
+  SlabArgs a{slab0, nslab, k, ctr};
+  LaunchScope ls("slab", st);
+  kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(x, y, z, a);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_slab(const T* x, const T* y, T* z, int M, int k, uint64_t slab0, uint32_t nslab,
+                        uint32_t* ctr, cudaStream_t st) {
+  switch (M) {
+    case 5: return launch_slab_m<T, 5>(x, y, z, k, slab0, nslab, ctr, st);
+    case 6: return launch_slab_m<T, 6>(x, y, z, k, slab0, nslab, ctr, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 }  // namespace
 
 // ---------------------------------------------------------------------------------------
+// Geometry: how the D axes are split.
+//   D <= 12 : single level -- tile of L = min(D, 8) low axes, k = D - L top axes direct.
+//   D >= 13 : two levels   -- slab of s = min(D, 14) axes (tile 8 + M = s - 8 middle axes,
+//             interpolated in L2), k = D - s top axes direct.
+// The unit of work distribution and sharding is one output slab (3^(L+M) entries).
+struct Geometry {
+  bool two_level;
+  int L, M, k;
+  uint64_t unit, nunits;
+};
+static Geometry geometry(int D) {
+  Geometry g;
+  g.two_level = D >= 13;
+  g.L = D < kTileL ? D : kTileL;
+  g.M = g.two_level ? (D < 14 ? D : 14) - kTileL : 0;
+  g.k = D - g.L - g.M;
+  g.unit = upow3(g.L + g.M);
+  g.nunits = upow3(g.k);
+  return g;
+}
+
 struct hc_plan_s {
   int D;
   hc_dtype dtype;
   int ngpu, rank;
-  int L, k;                       // tile axes, top (direct-split) axes
-  uint64_t nslab;                 // 3^k output slabs of 3^L entries
-  std::vector<uint64_t> cuts;     // ngpu+1 slab boundaries (equal cost)
+  Geometry g;
+  std::vector<uint64_t> cuts;     // ngpu+1 unit (slab) boundaries (equal cost)
+  uint32_t* ctr[3] = {nullptr, nullptr, nullptr};  // slab-engine counters (device, per stream slot)
   // host entry point workspace
   void* dx = nullptr;
   void* dy = nullptr;
   void* dz[2] = {nullptr, nullptr};
-  uint64_t chunk_slabs = 0;
+  uint64_t chunk_units = 0;
   cudaStream_t hs[2] = {nullptr, nullptr};
 };
 
@@ -212,16 +280,14 @@ static std::vector<uint64_t> compute_cuts(int k, int ngpu) {
   return cuts;
 }
 
-static inline int tile_axes(int D) { return D < kTileL ? D : kTileL; }
-
 extern "C" hc_status hc_shard_range(int D, int ngpu, int rank, uint64_t* zb, uint64_t* ze) {
   if (!zb || !ze) return HC_ERR_NULL;
   if (D < 1 || D > HC_MAX_D) return HC_ERR_INVALID_DIM;
-  const int L = tile_axes(D), k = D - L;
-  if (ngpu < 1 || rank < 0 || rank >= ngpu || (uint64_t)ngpu > upow3(k)) return HC_ERR_SHARD;
-  std::vector<uint64_t> cuts = compute_cuts(k, ngpu);
-  *zb = cuts[rank] * upow3(L);
-  *ze = cuts[rank + 1] * upow3(L);
+  const Geometry g = geometry(D);
+  if (ngpu < 1 || rank < 0 || rank >= ngpu || (uint64_t)ngpu > g.nunits) return HC_ERR_SHARD;
+  std::vector<uint64_t> cuts = compute_cuts(g.k, ngpu);
+  *zb = cuts[rank] * g.unit;
+  *ze = cuts[rank + 1] * g.unit;
   return HC_OK;
 }
 
@@ -233,19 +299,25 @@ extern "C" hc_status hc_plan_create(hc_plan_t* out, int D, hc_dtype dtype, int n
   if (ngpu < 1 || rank < 0 || rank >= ngpu) return HC_ERR_SHARD;
   hc_status ds = check_device();
   if (ds != HC_OK) return ds;
+  const Geometry g = geometry(D);
+  if ((uint64_t)ngpu > g.nunits) return HC_ERR_SHARD;
   auto* p = new hc_plan_s();
   p->D = D;
   p->dtype = dtype;
   p->ngpu = ngpu;
   p->rank = rank;
-  p->L = tile_axes(D);
-  p->k = D - p->L;
-  p->nslab = upow3(p->k);
-  if ((uint64_t)ngpu > p->nslab) {
-    delete p;
-    return HC_ERR_SHARD;
+  p->g = g;
+  p->cuts = compute_cuts(g.k, ngpu);
+  if (g.two_level) {
+    for (auto& c : p->ctr) {
+      if (cudaMalloc(&c, sizeof(uint32_t) * (1 + g.nunits)) != cudaSuccess) {
+        cudaGetLastError();
+        for (auto& c2 : p->ctr) cudaFree(c2);
+        delete p;
+        return HC_ERR_CAPACITY;
+      }
+    }
   }
-  p->cuts = compute_cuts(p->k, ngpu);
   *out = p;
   return HC_OK;
 }
@@ -256,6 +328,7 @@ extern "C" hc_status hc_plan_destroy(hc_plan_t p) {
   cudaFree(p->dy);
   cudaFree(p->dz[0]);
   cudaFree(p->dz[1]);
+  for (auto& c : p->ctr) cudaFree(c);
   for (auto& s : p->hs)
     if (s) cudaStreamDestroy(s);
   delete p;
@@ -265,29 +338,39 @@ extern "C" hc_status hc_plan_destroy(hc_plan_t p) {
 extern "C" hc_status hc_shard_info(hc_plan_t p, int rank, uint64_t* zb, uint64_t* ze) {
   if (!p || !zb || !ze) return HC_ERR_NULL;
   if (rank < 0 || rank >= p->ngpu) return HC_ERR_SHARD;
-  const uint64_t tile = upow3(p->L);
-  *zb = p->cuts[rank] * tile;
-  *ze = p->cuts[rank + 1] * tile;
+  *zb = p->cuts[rank] * p->g.unit;
+  *ze = p->cuts[rank + 1] * p->g.unit;
   return HC_OK;
 }
 
-static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, uint64_t s0, uint64_t s1,
-                           cudaStream_t st) {
-  if (s1 <= s0) return HC_OK;
-  cudaError_t e = launch_any(p->dtype, x, y, z, p->D, s0, p->nslab, s1 - s0, st);
+// units [u0, u1) of the plan's geometry into z (z points at unit u0)
+static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, uint64_t u0, uint64_t u1,
+                           cudaStream_t st, int slot) {
+  if (u1 <= u0) return HC_OK;
+  const Geometry& g = p->g;
+  cudaError_t e;
+  if (!g.two_level) {
+    e = launch_any(p->dtype, x, y, z, p->D, u0, g.nunits, u1 - u0, st);
+  } else if (p->dtype == HC_INT64) {
+    e = launch_slab<uint64_t>((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)z, g.M, g.k, u0,
+                              (uint32_t)(u1 - u0), p->ctr[slot], st);
+  } else {
+    e = launch_slab<double>((const double*)x, (const double*)y, (double*)z, g.M, g.k, u0, (uint32_t)(u1 - u0),
+                            p->ctr[slot], st);
+  }
   return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
 }
 
 extern "C" hc_status hc_convolve(hc_plan_t p, const void* x, const void* y, void* z, void* stream) {
   if (!p || !x || !y || !z) return HC_ERR_NULL;
   if (!aligned16(x) || !aligned16(y) || !aligned16(z)) return HC_ERR_ALIGN;
-  return run_range(p, x, y, z, 0, p->nslab, (cudaStream_t)stream);
+  return run_range(p, x, y, z, 0, p->g.nunits, (cudaStream_t)stream, 0);
 }
 
 extern "C" hc_status hc_convolve_sharded(hc_plan_t p, const void* x, const void* y, void* zs, void* stream) {
   if (!p || !x || !y || !zs) return HC_ERR_NULL;
   if (!aligned16(x) || !aligned16(y) || !aligned16(zs)) return HC_ERR_ALIGN;
-  return run_range(p, x, y, zs, p->cuts[p->rank], p->cuts[p->rank + 1], (cudaStream_t)stream);
+  return run_range(p, x, y, zs, p->cuts[p->rank], p->cuts[p->rank + 1], (cudaStream_t)stream, 0);
 }
 
 extern "C" hc_status hc_convolve_batched(int B, int D, hc_dtype dtype, const void* x, const void* y, void* z,
@@ -298,7 +381,7 @@ extern "C" hc_status hc_convolve_batched(int B, int D, hc_dtype dtype, const voi
   if (!aligned16(x) || !aligned16(y) || !aligned16(z)) return HC_ERR_ALIGN;
   hc_status ds = check_device();
   if (ds != HC_OK) return ds;
-  const int L = tile_axes(D);
+  const int L = D < kTileL ? D : kTileL;
   const uint64_t nslab = upow3(D - L);
   const uint64_t nitems = (uint64_t)B * nslab;
   if (nitems > 0x7fffffffull) return HC_ERR_INVALID_DIM;
@@ -310,7 +393,7 @@ extern "C" hc_status hc_convolve_host(hc_plan_t p, const void* xh, const void* y
   if (!p || !xh || !yh || !zh) return HC_ERR_NULL;
   const size_t esz = 8;
   const uint64_t nin = 1ull << p->D;
-  const uint64_t tile = upow3(p->L);
+  const uint64_t tile = p->g.unit;
   const uint64_t s0 = p->cuts[p->rank], s1 = p->cuts[p->rank + 1];
   cudaStream_t st = (cudaStream_t)stream;
   if (!p->dx) {
@@ -323,7 +406,7 @@ extern "C" hc_status hc_convolve_host(hc_plan_t p, const void* xh, const void* y
     if (cs < 1) cs = 1;
     if (cs > s1 - s0) cs = s1 - s0;
     if (cs < 1) cs = 1;
-    p->chunk_slabs = cs;
+    p->chunk_units = cs;
     for (int i = 0; i < 2; ++i) {
       if (cudaMalloc(&p->dz[i], cs * tile * esz) != cudaSuccess) {
         cudaGetLastError();
@@ -338,11 +421,11 @@ extern "C" hc_status hc_convolve_host(hc_plan_t p, const void* xh, const void* y
   cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
   cudaEventRecord(ready, st);
   int i = 0;
-  for (uint64_t c = s0; c < s1; c += p->chunk_slabs, i ^= 1) {
-    const uint64_t ce = c + p->chunk_slabs < s1 ? c + p->chunk_slabs : s1;
+  for (uint64_t c = s0; c < s1; c += p->chunk_units, i ^= 1) {
+    const uint64_t ce = c + p->chunk_units < s1 ? c + p->chunk_units : s1;
     cudaStream_t hs = p->hs[i];
     cudaStreamWaitEvent(hs, ready, 0);
-    hc_status r = run_range(p, p->dx, p->dy, p->dz[i], c, ce, hs);
+    hc_status r = run_range(p, p->dx, p->dy, p->dz[i], c, ce, hs, 1 + i);
     if (r != HC_OK) return r;
     if (cudaMemcpyAsync((char*)zh + (c - s0) * tile * esz, p->dz[i], (ce - c) * tile * esz,
                         cudaMemcpyDeviceToHost, hs) != cudaSuccess)

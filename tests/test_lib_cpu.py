@@ -65,10 +65,17 @@ def _slab_cost(t, k):
     return 1 + 2 ** ones
 
 
+def _unit_axes(D):
+    # DESIGN.md §4 geometry: single level (tile of min(D, 8) axes) for D <= 12, otherwise a
+    # two-level slab of min(D, 14) axes; the remaining top axes use the direct split
+    return min(D, 8) if D <= 12 else min(D, 14)
+
+
 @pytest.mark.parametrize("D", [9, 12, 16, 20, 22])
 @pytest.mark.parametrize("ngpu", [1, 2, 3, 4, 8])
 def test_shard_ranges_partition(hc, D, ngpu):
-    if ngpu > 3 ** (D - 8):
+    s = _unit_axes(D)
+    if ngpu > 3 ** (D - s):
         with pytest.raises(hc.HCError):
             hc.shard_range(D, ngpu, 0)
         return
@@ -76,12 +83,12 @@ def test_shard_ranges_partition(hc, D, ngpu):
     assert ranges[0][0] == 0 and ranges[-1][1] == 3 ** D
     for (b0, e0), (b1, e1) in zip(ranges, ranges[1:]):
         assert e0 == b1
-    tile = 3 ** 8
+    tile = 3 ** s
     for b, e in ranges:
         assert b % tile == 0 and e % tile == 0 and e > b
     if D <= 16 and ngpu > 1:
         # balance: per-rank cost within one heaviest slab of the ideal share
-        k = D - 8
+        k = D - s
         costs = [sum(_slab_cost(t, k) for t in range(b // tile, e // tile)) for b, e in ranges]
         ideal = sum(costs) / ngpu
         assert max(costs) - ideal <= 1 + 2 ** k
