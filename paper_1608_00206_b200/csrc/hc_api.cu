@@ -5,7 +5,10 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -13,6 +16,7 @@
 #include "../../include/hc.h"
 #include "hc_common.cuh"
 #include "hc_tile.cuh"
+#include "hc_slab.cuh"
 
 using namespace hc;
 
@@ -122,6 +126,62 @@ hc_status check_device() {
   return ok ? HC_OK : HC_ERR_DEVICE;
 }
 
+// ---- 8-axis tiles: single level (tile8_kernel) and two levels (prep + slab8_kernel) ----
+template <class T>
+cudaError_t launch_tile8(const T* x, const T* y, T* z, int D, uint64_t slab0, uint64_t nslab, uint64_t nitems,
+                         cudaStream_t st) {
+  auto kern = tile8_kernel<T>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T8Cfg<T>::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  LaunchScope ls("tile", st);
+  kern<<<(unsigned)nitems, T8_NT, T8Cfg<T>::SMEM, st>>>(x, y, z, D, slab0, nslab);
+  return cudaGetLastError();
+}
+
+template <class T, int M>
+cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st) {
+  auto kern = slab8_kernel<T, M>;
+  static int grid_max = 0;
+  if (!grid_max) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T8Cfg<T>::SMEM);
+    if (e != cudaSuccess) return e;
+    int occ = 0, dev = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T8_NT, T8Cfg<T>::SMEM);
+    if (e != cudaSuccess) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    grid_max = occ * sms;
+  }
+  const uint64_t items = (uint64_t)a.nslab * (upow3(M) + upow3(8) / P2W);
+  const unsigned grid = (unsigned)(items < (uint64_t)grid_max ? items : (uint64_t)grid_max);
+  cudaError_t e = cudaMemsetAsync(a.ctr, 0, sizeof(uint32_t) * (1 + (size_t)a.nslab), st);
+  if (e != cudaSuccess) return e;
+  {
+    LaunchScope lp("prep", st);
+    dim3 pg((unsigned)upow3(M), 1u << a.k, 2);
+    prep_kernel<T, M><<<pg, 256, 0, st>>>(x, y, xu, yu);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  LaunchScope ls("slab", st);
+  kern<<<grid, T8_NT, T8Cfg<T>::SMEM, st>>>(xu, yu, z, a);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_slab8(const T* x, const T* y, T* z, T* xu, T* yu, int M, const SlabArgs& a, cudaStream_t st) {
+  switch (M) {
+    case 5: return launch_slab8_m<T, 5>(x, y, z, xu, yu, a, st);
+    case 6: return launch_slab8_m<T, 6>(x, y, z, xu, yu, a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 // ---- launch of the tile engine for L = min(D, 8) --------------------------------------
 template <class T, int C, int B, int A>
 cudaError_t launch_tile_cfg(const T* x, const T* y, T* z, int D, uint64_t slab0, uint64_t nslab,
@@ -160,7 +220,7 @@ cudaError_t launch_tile(const T* x, const T* y, T* z, int D, uint64_t slab0, uin
     case 5: return launch_tile_cfg<T, 3, 2, 0>(x, y, z, D, slab0, nslab, nitems, st);
     case 6: return launch_tile_cfg<T, 3, 3, 0>(x, y, z, D, slab0, nslab, nitems, st);
     case 7: return launch_tile_cfg<T, 3, 3, 1>(x, y, z, D, slab0, nslab, nitems, st);
-    default: return launch_tile_cfg<T, 3, 3, 2>(x, y, z, D, slab0, nslab, nitems, st);
+    default: return launch_tile8<T>(x, y, z, D, slab0, nslab, nitems, st);
   }
 }
 
@@ -170,44 +230,6 @@ cudaError_t launch_any(hc_dtype dt, const void* x, const void* y, void* z, int D
     return launch_tile<uint64_t>((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)z, D, slab0, nslab,
                                  nitems, st);
   return launch_tile<double>((const double*)x, (const double*)y, (double*)z, D, slab0, nslab, nitems, st);
-}
-
-// ---- launch of the two-level slab engine -----------------------------------------------
-template <class T, int M>
-cudaError_t launch_slab_m(const T* x, const T* y, T* z, int k, uint64_t slab0, uint32_t nslab, uint32_t* ctr,
-                          cudaStream_t st) {
-  using Cfg = TileCfg<T, 3, 3, 2>;
-  auto kern = slab_kernel<T, 3, 3, 2, M>;
-  static int grid_max = 0;
-  if (!grid_max) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    if (e != cudaSuccess) return e;
-    int occ = 0, dev = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NT, Cfg::SMEM);
-    if (e != cudaSuccess) return e;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (occ < 1) return cudaErrorInvalidConfiguration;
-    grid_max = occ * sms;
-  }
-  const uint64_t items = (uint64_t)nslab * (upow3(M) + upow3(Cfg::L) / P2W);
-  const unsigned grid = (unsigned)(items < (uint64_t)grid_max ? items : (uint64_t)grid_max);
-  cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * (1 + (size_t)nslab), st);
-  if (e != cudaSuccess) return e;
-  SlabArgs a{slab0, nslab, k, ctr};
-  LaunchScope ls("slab", st);
-  kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(x, y, z, a);
-  return cudaGetLastError();
-}
-
-template <class T>
-cudaError_t launch_slab(const T* x, const T* y, T* z, int M, int k, uint64_t slab0, uint32_t nslab,
-                        uint32_t* ctr, cudaStream_t st) {
-  switch (M) {
-    case 5: return launch_slab_m<T, 5>(x, y, z, k, slab0, nslab, ctr, st);
-    case 6: return launch_slab_m<T, 6>(x, y, z, k, slab0, nslab, ctr, st);
-    default: return cudaErrorInvalidValue;
-  }
 }
 
 }  // namespace
@@ -227,7 +249,11 @@ static Geometry geometry(int D) {
   Geometry g;
   g.two_level = D >= 13;
   g.L = D < kTileL ? D : kTileL;
-  g.M = g.two_level ? (D < 14 ? D : 14) - kTileL : 0;
+  // slab axes s = min(D, 14) (38 MB fp64 slabs fit twice in the 126 MB L2); HC_SLAB_AXES
+  // overrides it for experiments (13 or 14)
+  static const int s_env = getenv("HC_SLAB_AXES") ? atoi(getenv("HC_SLAB_AXES")) : 14;
+  const int smax = (s_env == 13 || s_env == 14) ? s_env : 14;
+  g.M = g.two_level ? (D < smax ? D : smax) - kTileL : 0;
   g.k = D - g.L - g.M;
   g.unit = upow3(g.L + g.M);
   g.nunits = upow3(g.k);
@@ -241,6 +267,10 @@ struct hc_plan_s {
   Geometry g;
   std::vector<uint64_t> cuts;     // ngpu+1 unit (slab) boundaries (equal cost)
   uint32_t* ctr[3] = {nullptr, nullptr, nullptr};  // slab-engine counters (device, per stream slot)
+  void* xu = nullptr;             // two-level: middle-axes-evaluated input slices (prep kernel)
+  void* yu = nullptr;
+  std::mutex order_mu;
+  std::map<std::pair<uint64_t, uint64_t>, uint32_t*> orders;  // [u0,u1) -> device processing order
   // host entry point workspace
   void* dx = nullptr;
   void* dy = nullptr;
@@ -308,7 +338,7 @@ extern "C" hc_status hc_plan_create(hc_plan_t* out, int D, hc_dtype dtype, int n
   p->rank = rank;
   p->g = g;
   p->cuts = compute_cuts(g.k, ngpu);
-  if (g.two_level) {
+  {
     for (auto& c : p->ctr) {
       if (cudaMalloc(&c, sizeof(uint32_t) * (1 + g.nunits)) != cudaSuccess) {
         cudaGetLastError();
@@ -316,6 +346,14 @@ extern "C" hc_status hc_plan_create(hc_plan_t* out, int D, hc_dtype dtype, int n
         delete p;
         return HC_ERR_CAPACITY;
       }
+    }
+  }
+  if (g.two_level) {
+    const size_t bytes = sizeof(double) * (size_t)(1ull << g.k) * upow3(g.M) * 256;
+    if (cudaMalloc(&p->xu, bytes) != cudaSuccess || cudaMalloc(&p->yu, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      hc_plan_destroy(p);
+      return HC_ERR_CAPACITY;
     }
   }
   *out = p;
@@ -329,6 +367,9 @@ extern "C" hc_status hc_plan_destroy(hc_plan_t p) {
   cudaFree(p->dz[0]);
   cudaFree(p->dz[1]);
   for (auto& c : p->ctr) cudaFree(c);
+  cudaFree(p->xu);
+  cudaFree(p->yu);
+  for (auto& kv : p->orders) cudaFree(kv.second);
   for (auto& s : p->hs)
     if (s) cudaStreamDestroy(s);
   delete p;
@@ -343,6 +384,38 @@ extern "C" hc_status hc_shard_info(hc_plan_t p, int rank, uint64_t* zb, uint64_t
   return HC_OK;
 }
 
+// Processing order of the slabs [u0, u1) for the slab engine: sorted by the number of
+// direct-split pairs 2^{#1(t_T)} so that consecutive slabs cost the same and a pass-2 item
+// rarely waits for a slow pass-1 item of its slab.  Cached per range on the plan.
+static const uint32_t* slab_order(hc_plan_t p, uint64_t u0, uint64_t u1) {
+  std::lock_guard<std::mutex> lk(p->order_mu);
+  auto key = std::make_pair(u0, u1);
+  auto it = p->orders.find(key);
+  if (it != p->orders.end()) return it->second;
+  const uint64_t n = u1 - u0;
+  std::vector<std::pair<int, uint32_t>> v(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t t = u0 + i;
+    int ones = 0;
+    for (int a = 0; a < p->g.k; ++a) {
+      ones += (t % 3 == 1);
+      t /= 3;
+    }
+    v[i] = {ones, (uint32_t)i};
+  }
+  std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  std::vector<uint32_t> h(n);
+  for (uint64_t i = 0; i < n; ++i) h[i] = v[i].second;
+  uint32_t* d = nullptr;
+  if (cudaMalloc(&d, sizeof(uint32_t) * n) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  if (cudaMemcpy(d, h.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  p->orders[key] = d;
+  return d;
+}
+
 // units [u0, u1) of the plan's geometry into z (z points at unit u0)
 static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, uint64_t u0, uint64_t u1,
                            cudaStream_t st, int slot) {
@@ -351,12 +424,17 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
   cudaError_t e;
   if (!g.two_level) {
     e = launch_any(p->dtype, x, y, z, p->D, u0, g.nunits, u1 - u0, st);
-  } else if (p->dtype == HC_INT64) {
-    e = launch_slab<uint64_t>((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)z, g.M, g.k, u0,
-                              (uint32_t)(u1 - u0), p->ctr[slot], st);
   } else {
-    e = launch_slab<double>((const double*)x, (const double*)y, (double*)z, g.M, g.k, u0, (uint32_t)(u1 - u0),
-                            p->ctr[slot], st);
+    const uint32_t* order = slab_order(p, u0, u1);
+    if (!order) return HC_ERR_CAPACITY;
+    static const int dbg = getenv("HC_DEBUG_SKIP") ? atoi(getenv("HC_DEBUG_SKIP")) : 0;
+    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg};
+    if (p->dtype == HC_INT64)
+      e = launch_slab8<uint64_t>((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)z, (uint64_t*)p->xu,
+                                 (uint64_t*)p->yu, g.M, a, st);
+    else
+      e = launch_slab8<double>((const double*)x, (const double*)y, (double*)z, (double*)p->xu, (double*)p->yu,
+                               g.M, a, st);
   }
   return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
 }

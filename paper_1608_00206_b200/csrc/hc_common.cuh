@@ -85,6 +85,12 @@ __device__ __forceinline__ void inv_reg(T* a) {
   if constexpr (N > 0) inv_axis<N, 0, T>(a);
 }
 
+// exchange with lane ^ 1 (all 32 lanes of the warp must participate)
+__device__ __forceinline__ double shfl_xor1(double v) { return __shfl_xor_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ uint64_t shfl_xor1(uint64_t v) {
+  return (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)v, 1);
+}
+
 // streaming (evict-first) 8-byte global store
 __device__ __forceinline__ void st_cs(uint64_t* p, uint64_t v) {
   asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

@@ -52,46 +52,66 @@ __device__ __forceinline__ void p1_stage(const T* __restrict__ xb, const T* __re
                                          const uint32_t* s_off, int nsl, T* P) {
   using Cfg = TileCfg<T, C, B, A>;
   constexpr int P3B = ipow3(B), P2A = 1 << A, P2C = 1 << C, NLINE = P2A * P2C;
-  for (int wl = threadIdx.x; wl < 2 * NLINE; wl += Cfg::NT) {
-  const int op = wl / NLINE, r = wl - op * NLINE;
-  const int bA = r / P2C, blo = r - bA * P2C;
-  const T* src = (op ? yb : xb) + blo + (P2C << B) * bA;
-  T in[1 << B];
+  constexpr int NB = 1 << B;
+  // Two lanes per line when the line threads fill whole warps in one pass (L = 7, 8):
+  // lanes 2w and 2w+1 share line w, each gathers half of the 2^B inputs, then they swap.
+  // Otherwise (small tiles) one thread per line.
+  constexpr bool TWO = (4 * NLINE) % 32 == 0 && 4 * NLINE <= Cfg::NT;
+  constexpr int HB = TWO ? NB / 2 : NB;
+  for (int t = threadIdx.x; t < (TWO ? 4 : 2) * NLINE; t += Cfg::NT) {
+    const int wl = TWO ? (t >> 1) : t, half = TWO ? (t & 1) : 0;
+    const int op = wl / NLINE, r = wl - op * NLINE;
+    const int bA = r / P2C, blo = r - bA * P2C;
+    const T* src = (op ? yb : xb) + blo + (P2C << B) * bA + P2C * HB * half;
+    T in[HB];
 #pragma unroll
-  for (int j = 0; j < (1 << B); ++j) in[j] = T(0);
-  // nsl is a power of two; take slices four at a time so 4 * 2^B loads are in flight
-  if (nsl >= 4) {
-    for (int q = 0; q < nsl; q += 4) {
-      T v[4][1 << B];
+    for (int j = 0; j < HB; ++j) in[j] = T(0);
+    // nsl is a power of two; take slices four at a time so 4 * 2^(B-1) loads are in flight
+    if (nsl >= 4) {
+      for (int q = 0; q < nsl; q += 4) {
+        T v[4][HB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const T* sp = src + s_off[q + u];
+        for (int u = 0; u < 4; ++u) {
+          const T* sp = src + s_off[q + u];
 #pragma unroll
-        for (int j = 0; j < (1 << B); ++j) v[u][j] = __ldg(sp + P2C * j);
+          for (int j = 0; j < HB; ++j) v[u][j] = __ldg(sp + P2C * j);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int j = 0; j < HB; ++j) in[j] = Ar<T>::add(in[j], v[u][j]);
+      }
+    } else {
+      T v[2][HB];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const T* sp = src + s_off[u < nsl ? u : 0];
+#pragma unroll
+        for (int j = 0; j < HB; ++j) v[u][j] = (u < nsl) ? __ldg(sp + P2C * j) : T(0);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int j = 0; j < (1 << B); ++j) in[j] = Ar<T>::add(in[j], v[u][j]);
+        for (int j = 0; j < HB; ++j) in[j] = Ar<T>::add(in[j], v[u][j]);
     }
-  } else {
-    T v[2][1 << B];
+    T full[NB];
+    if constexpr (TWO) {
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const T* sp = src + s_off[u < nsl ? u : 0];
+      for (int j = 0; j < HB; ++j) {
+        const T o = shfl_xor1(in[j]);
+        full[j] = half ? o : in[j];
+        full[j + HB] = half ? in[j] : o;
+      }
+    } else {
 #pragma unroll
-      for (int j = 0; j < (1 << B); ++j) v[u][j] = (u < nsl) ? __ldg(sp + P2C * j) : T(0);
+      for (int j = 0; j < NB; ++j) full[j] = in[j];
     }
+    T out[ipow3(B)];
+    fwd_reg<B, T>(full, out);
+    T* dst = P + op * Cfg::NP + r * P3B;
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int j = 0; j < (1 << B); ++j) in[j] = Ar<T>::add(in[j], v[u][j]);
-  }
-  T out[ipow3(B)];
-  fwd_reg<B, T>(in, out);
-  T* dst = P + op * Cfg::NP + r * P3B;
-#pragma unroll
-  for (int e = 0; e < P3B; ++e) dst[e] = out[e];
+    for (int e = 0; e < P3B; ++e)
+      if (!TWO || (e & 1) == half) dst[e] = out[e];
   }
 }
 
@@ -245,6 +265,8 @@ struct SlabArgs {
   uint32_t nslab;      // slabs in this launch
   int k;               // top axes
   uint32_t* ctr;       // [0] = work counter, [1 + j] = pass-1 tiles done in slab j
+  const uint32_t* order;  // processing position j -> slab offset within the launch (cost-sorted)
+  int debug_skip;      // timing experiments only (HC_DEBUG_SKIP): 1 = no pass 2, 2 = no pass 1
 };
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
@@ -292,60 +314,6 @@ __device__ __forceinline__ void p2_item(T* __restrict__ zs, uint32_t c, T* sm, i
     inv_reg<HI, T>(v);
 #pragma unroll
     for (int e = 0; e < NHI; ++e) st_cs(zs + (uint64_t)(e * NLO + el) * ROW + col0 + pos, v[e]);
-  }
-}
-
-template <class T, int C, int B, int A, int M>
-__global__ void __launch_bounds__(TileCfg<T, C, B, A>::NT)
-slab_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z, SlabArgs args) {
-  using Cfg = TileCfg<T, C, B, A>;
-  constexpr int L = Cfg::L, NT = Cfg::NT;
-  constexpr uint32_t N1 = (uint32_t)ipow3(M);                // pass-1 items per slab
-  constexpr uint32_t N2 = (uint32_t)(ipow3(L) / P2W);        // pass-2 items per slab
-  constexpr uint64_t SLAB = upow3(M + L);
-  static_assert(ipow3(L) % P2W == 0, "pass-2 chunking");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sm = reinterpret_cast<T*>(smem_raw);
-  __shared__ uint32_t s_item;
-  const uint32_t ns = args.nslab;
-  const uint64_t total = (uint64_t)ns * (N1 + N2);
-  while (true) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_item = atomicAdd(args.ctr, 1u);
-    __syncthreads();
-    const uint64_t q = s_item;
-    if (q >= total) break;
-    // decode: P1(0) | [P1(j+1) P2(j)] for j = 0..ns-2 | P2(ns-1)
-    bool is_p1;
-    uint32_t j, r;
-    if (q < N1) {
-      is_p1 = true; j = 0; r = (uint32_t)q;
-    } else {
-      const uint64_t q2 = q - N1;
-      const uint32_t pr = (uint32_t)(q2 / (N1 + N2));
-      const uint32_t rr = (uint32_t)(q2 - (uint64_t)pr * (N1 + N2));
-      if (pr + 1 < ns) {
-        if (rr < N1) { is_p1 = true; j = pr + 1; r = rr; }
-        else { is_p1 = false; j = pr; r = rr - N1; }
-      } else {
-        is_p1 = false; j = pr; r = rr;
-      }
-    }
-    T* zs = z + (uint64_t)j * SLAB;
-    if (is_p1) {
-      p1_tile<T, C, B, A, false>(x, y, zs + (uint64_t)r * upow3(L), args.k, M, args.slab0 + j, r, sm);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(args.ctr + 1 + j, 1u);
-      }
-    } else {
-      if (threadIdx.x == 0) {
-        while (ld_acquire(args.ctr + 1 + j) < N1) __nanosleep(256);
-      }
-      __syncthreads();
-      p2_item<T, M, L>(zs, r, sm, NT);
-    }
   }
 }
 
