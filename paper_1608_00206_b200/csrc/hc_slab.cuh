@@ -248,9 +248,15 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   const uint64_t pol_in = policy_evict_first();   // middle-axes tables are streamed
   const uint64_t pol_keep = policy_evict_last();  // pass-1 tiles wait in L2 for pass 2
   const uint64_t stride = upow3(M) * 256;
+  // claim one item ahead so the atomic's latency overlaps the current item (the claim order
+  // -- and with it the deadlock argument -- is unchanged)
+  uint32_t nq = threadIdx.x == 0 ? atomicAdd(args.ctr, 1u) : 0u;
   while (true) {
     __syncthreads();
-    if (threadIdx.x == 0) s_item = atomicAdd(args.ctr, 1u);
+    if (threadIdx.x == 0) {
+      s_item = nq;
+      nq = atomicAdd(args.ctr, 1u);
+    }
     __syncthreads();
     const uint64_t q = s_item;
     if (q >= total) break;
