@@ -37,15 +37,32 @@ __device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
 __device__ __forceinline__ void st_hint(uint64_t* p, uint64_t v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
 }
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src), "l"(pol)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(smem_u32(b)),
+               "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// TMA 1-D bulk copy global -> shared, completion on an mbarrier (complete_tx), L2 policy
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 
 constexpr int T8_NT = 243;        // threads per tile CTA
 constexpr int T8_NLINE = 72;      // F1 lines per operand: (e_A in 9) x (b_lo in 8)
@@ -56,6 +73,7 @@ template <class T>
 struct T8Cfg {
   static constexpr size_t SMEM = sizeof(T) * (size_t)(2 * T8_PSZ + T8_NRAW * T8_RAW);
   static_assert(2 * T8_PSZ >= 6561, "tile exchange buffer aliases the two stages");
+  static_assert(2 * T8_PSZ >= P2Cfg<6>::SIZE, "pass-2 buffer aliases the two stages");
 };
 
 // Prep kernel (two-level only): evaluate the M middle axes of every input slice once per
@@ -79,14 +97,29 @@ __global__ void __launch_bounds__(256) prep_kernel(const T* __restrict__ x, cons
   *dst = acc;
 }
 
-// issue the cp.async copies of the raw slices of one pair into raw stage R
+// raw-slice staging: T8_NRAW stages, each filled by two TMA bulk copies (x slice, y slice)
+// and completed on its mbarrier.  seq counts fills over the CTA's lifetime (same value in
+// every thread) so the parity of each stage's barrier is known.
+struct RawRing {
+  uint64_t* bar;     // [T8_NRAW] in shared memory
+  uint32_t seq;      // fills issued so far
+  uint32_t done;     // fills consumed so far
+};
 template <class T>
-__device__ __forceinline__ void t8_prefetch(const T* sx, const T* sy, T* R, uint64_t pol) {
-  constexpr int CH = 256 * (int)sizeof(T) / 16;   // 16-byte chunks per slice (128)
-  for (int c = threadIdx.x; c < 2 * CH; c += T8_NT) {
-    const int op = c / CH, cc = c - op * CH;
-    cp_async16(R + op * 256 + cc * (16 / (int)sizeof(T)), (op ? sy : sx) + cc * (16 / (int)sizeof(T)), pol);
+__device__ __forceinline__ void t8_issue(RawRing& rr, const T* sx, const T* sy, T* R, uint64_t pol) {
+  const uint32_t st = rr.seq % T8_NRAW;
+  if (threadIdx.x == 0) {
+    mbar_arrive_tx(&rr.bar[st], 2 * 256 * sizeof(T));
+    tma_load_1d(R + st * T8_RAW, sx, 256 * sizeof(T), &rr.bar[st], pol);
+    tma_load_1d(R + st * T8_RAW + 256, sy, 256 * sizeof(T), &rr.bar[st], pol);
   }
+  ++rr.seq;
+}
+__device__ __forceinline__ uint32_t t8_wait(RawRing& rr) {
+  const uint32_t st = rr.done % T8_NRAW;
+  mbar_wait(&rr.bar[st], (rr.done / T8_NRAW) & 1);
+  ++rr.done;
+  return st;
 }
 
 // stage F1 of one pair: raw slices R -> P (line threads tid < 144)
@@ -116,8 +149,8 @@ __device__ __forceinline__ void t8_f1(const T* R, T* P, int tid, uint32_t lbase,
 // One pass-1 tile.  sx0/sy0 + iT*stride are the raw x / y slices of pair (iT, jT).
 template <class T, bool FINAL>
 __device__ __forceinline__ void tile8(const T* __restrict__ sx0, const T* __restrict__ sy0, uint64_t stride,
-                                      T* __restrict__ zt, int k, uint64_t tT, T* sm, uint64_t pol_in,
-                                      uint64_t pol_out) {
+                                      T* __restrict__ zt, int k, uint64_t tT, T* sm, RawRing& rr,
+                                      uint64_t pol_in, uint64_t pol_out) {
   T* P = sm;                          // [2][T8_PSZ]
   T* R = sm + 2 * T8_PSZ;             // [T8_NRAW][T8_RAW]
   T* S = sm;                          // [9][27][27] after the pair loop (aliases P)
@@ -146,26 +179,23 @@ __device__ __forceinline__ void tile8(const T* __restrict__ sx0, const T* __rest
   auto prefetch_next = [&]() {
     if (npf < npairs) {
       const uint64_t iT = base | s_pf, jT = base | (freeb & ~s_pf);
-      t8_prefetch<T>(sx0 + iT * stride, sy0 + jT * stride, R + (npf % T8_NRAW) * T8_RAW, pol_in);
+      t8_issue<T>(rr, sx0 + iT * stride, sy0 + jT * stride, R, pol_in);
       s_pf = (s_pf - freeb) & freeb;
       ++npf;
     }
-    cp_async_commit();  // (possibly empty) group per slot keeps the wait counts uniform
   };
 
-  __syncthreads();      // previous users of sm are done
+  __syncthreads();      // previous users of sm (and of the raw stages) are done
   prefetch_next();      // pair 0
   prefetch_next();      // pair 1
-  cp_async_wait<1>();   // pair 0 landed (own copies)
-  __syncthreads();      // ... and everyone's
-  t8_f1<T>(R, P, tid, lbase, lfree);
+  t8_f1<T>(R + t8_wait(rr) * T8_RAW, P, tid, lbase, lfree);
   __syncthreads();
 
   T acc[27];
 #pragma unroll
   for (int i = 0; i < 27; ++i) acc[i] = T(0);
   for (int p = 0; p < npairs; ++p) {
-    prefetch_next();  // pair p + 2
+    prefetch_next();  // pair p + 2 (its stage was last read by F1(p - 1), before a barrier)
     {
       // base values of (e_A, e_B): one line per b_lo, then C-axes forward fused with product
       const T* fx = P + (p & 1) * T8_PSZ;
@@ -179,14 +209,9 @@ __device__ __forceinline__ void tile8(const T* __restrict__ sx0, const T* __rest
       }
       fwd_mul_acc<3, T>(xt, yt, acc);
     }
-    if (p + 1 < npairs) {
-      cp_async_wait<1>();   // pair p + 1 landed (pair p + 2 may be in flight)
-      __syncthreads();
-      t8_f1<T>(R + ((p + 1) % T8_NRAW) * T8_RAW, P + ((p + 1) & 1) * T8_PSZ, tid, lbase, lfree);
-    }
+    if (p + 1 < npairs) t8_f1<T>(R + t8_wait(rr) * T8_RAW, P + ((p + 1) & 1) * T8_PSZ, tid, lbase, lfree);
     __syncthreads();
   }
-  cp_async_wait<0>();
 
   // a4: inverse on the C register axes, then B (SMEM exchange), then A + store (a6)
   inv_reg<3, T>(acc);
@@ -222,12 +247,19 @@ template <class T>
 __global__ void __launch_bounds__(T8_NT, 2)
 tile8_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z, int D, uint64_t slab0,
              uint64_t nslab) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
+  __shared__ __align__(8) uint64_t raw_bar[T8_NRAW];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < T8_NRAW; ++i) mbar_init(&raw_bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  RawRing rr{raw_bar, 0, 0};
   const uint64_t w = blockIdx.x;
   const uint64_t b = w / nslab;
   const uint64_t tT = slab0 + (w - b * nslab);
-  tile8<T, true>(x + (b << D), y + (b << D), 256, z + w * 6561ull, D - 8, tT, sm, policy_evict_last(), 0);
+  tile8<T, true>(x + (b << D), y + (b << D), 256, z + w * 6561ull, D - 8, tT, sm, rr, policy_evict_last(), 0);
 }
 
 // Two-level persistent kernel: pass-1 items (slab j, e_U) and pass-2 items (slab j, 9
@@ -240,9 +272,16 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   constexpr uint32_t N1 = (uint32_t)ipow3(M);
   constexpr uint32_t N2 = (uint32_t)(ipow3(8) / P2W);
   constexpr uint64_t SLAB = upow3(M + 8);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   __shared__ uint32_t s_item;
+  __shared__ __align__(8) uint64_t raw_bar[T8_NRAW];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < T8_NRAW; ++i) mbar_init(&raw_bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  RawRing rr{raw_bar, 0, 0};
   const uint32_t ns = args.nslab;
   const uint64_t total = (uint64_t)ns * (N1 + N2);
   const uint64_t pol_in = policy_evict_first();   // middle-axes tables are streamed
@@ -283,7 +322,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
         continue;
       }
       tile8<T, false>(xu + (uint64_t)r * 256, yu + (uint64_t)r * 256, stride, zs + (uint64_t)r * 6561ull, args.k,
-                      args.slab0 + loc, sm, pol_in, pol_keep);
+                      args.slab0 + loc, sm, rr, pol_in, pol_keep);
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence();

@@ -286,11 +286,21 @@ template <> __device__ __forceinline__ uint64_t ld_cg<uint64_t>(const uint64_t* 
   return v;
 }
 
-// pass-2 item: columns [c*P2W, c*P2W + P2W) of slab zs (3^M rows of 3^L)
+// pass-2 item: columns [c*P2W, c*P2W + P2W) of slab zs (3^M rows of 3^L).  SMEM buffer
+// layout: (e_hi, e_lo, pos) at e_hi * P2S + e_lo * P2W + pos with P2S = 9 (mod 16), so the
+// round-1 stores (lanes = (e_hi, pos)) and round-2 loads (lanes = (e_lo, pos)) are both
+// free of bank conflicts.
+template <int M>
+struct P2Cfg {
+  static constexpr int LO = M < 3 ? M : 3, HI = M - LO;
+  static constexpr int NLO = ipow3(LO), NHI = ipow3(HI);
+  static constexpr int P2S = NLO * P2W + ((9 - NLO * P2W) % 16 + 16) % 16;
+  static constexpr int SIZE = NHI * P2S;
+};
 template <class T, int M, int L>
 __device__ __forceinline__ void p2_item(T* __restrict__ zs, uint32_t c, T* sm, int nthreads) {
-  constexpr int LO = M < 3 ? M : 3, HI = M - LO;
-  constexpr int NLO = ipow3(LO), NHI = ipow3(HI);
+  using Q = P2Cfg<M>;
+  constexpr int LO = Q::LO, HI = Q::HI, NLO = Q::NLO, NHI = Q::NHI, P2S = Q::P2S;
   constexpr uint64_t ROW = upow3(L);
   const int tid = threadIdx.x;
   const uint64_t col0 = (uint64_t)c * P2W;
@@ -302,7 +312,7 @@ __device__ __forceinline__ void p2_item(T* __restrict__ zs, uint32_t c, T* sm, i
     for (int e = 0; e < NLO; ++e) v[e] = ld_cg(zs + (uint64_t)(eh * NLO + e) * ROW + col0 + pos);
     inv_reg<LO, T>(v);
 #pragma unroll
-    for (int e = 0; e < NLO; ++e) sm[(eh * NLO + e) * P2W + pos] = v[e];
+    for (int e = 0; e < NLO; ++e) sm[eh * P2S + e * P2W + pos] = v[e];
   }
   __syncthreads();
   // round 2: thread (e_lo, pos) interpolates over HI axes and stores the final values
@@ -310,7 +320,7 @@ __device__ __forceinline__ void p2_item(T* __restrict__ zs, uint32_t c, T* sm, i
     const int el = w / P2W, pos = w - el * P2W;
     T v[NHI];
 #pragma unroll
-    for (int e = 0; e < NHI; ++e) v[e] = sm[(e * NLO + el) * P2W + pos];
+    for (int e = 0; e < NHI; ++e) v[e] = sm[e * P2S + el * P2W + pos];
     inv_reg<HI, T>(v);
 #pragma unroll
     for (int e = 0; e < NHI; ++e) st_cs(zs + (uint64_t)(e * NLO + el) * ROW + col0 + pos, v[e]);
