@@ -213,6 +213,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of oracle work per reference step")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo lets several ranks share one GPU (testing the N > 1 path on one device)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -226,11 +228,17 @@ def main():
     import torch
     import paper_1608_00206_b200.hc as hc
 
-    torch.cuda.set_device(local_rank)
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local_rank % max(ndev, 1))
     dist = None
+    dev = "cuda"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
+            dev = "cpu"
 
     wl = args.workload
     w = WORKLOADS[wl]
@@ -275,7 +283,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
 
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(local_rank % max(ndev, 1))
     sampler.start()
     time.sleep(0.3)
     hc.prof_reset()
@@ -301,7 +309,7 @@ def main():
         ktime, kcount = hc.prof_read(prof_name)
     hc.prof_reset()
 
-    t_max, k_avg = reduce_max([t_ms, ktime / max(kcount, 1)], dist)
+    t_max, k_avg = reduce_max([t_ms, ktime / max(kcount, 1)], dist, device=dev)
     ms_per_step = t_max / args.steps
     value = n_total / (ms_per_step / 1e3)
 
@@ -331,7 +339,7 @@ def main():
             t0 = time.perf_counter()
             plan.convolve_host(xh, yh, zh)
             ts.append(time.perf_counter() - t0)
-        tm = reduce_max([statistics.median(ts)], dist)[0]
+        tm = reduce_max([statistics.median(ts)], dist, device=dev)[0]
         e2e = {"value": n_total / tm, "unit": UNIT, "h2d_bytes_per_step": in_bytes,
                "d2h_bytes_per_step": n_total * 8, "seconds_per_step": tm,
                "path": "hc_convolve_host (pinned host x,y -> device -> pinned host z, chunked D2H overlapped)"}
