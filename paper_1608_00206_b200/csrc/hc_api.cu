@@ -428,7 +428,8 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
     const uint32_t* order = slab_order(p, u0, u1);
     if (!order) return HC_ERR_CAPACITY;
     static const int dbg = getenv("HC_DEBUG_SKIP") ? atoi(getenv("HC_DEBUG_SKIP")) : 0;
-    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg};
+    static const int lag = getenv("HC_SLAB_LAG") ? atoi(getenv("HC_SLAB_LAG")) : 1;
+    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg, (uint32_t)(lag < 1 ? 1 : lag)};
     if (p->dtype == HC_INT64)
       e = launch_slab8<uint64_t>((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)z, (uint64_t*)p->xu,
                                  (uint64_t*)p->yu, g.M, a, st);

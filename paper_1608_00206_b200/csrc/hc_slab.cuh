@@ -299,19 +299,23 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
     __syncthreads();
     const uint64_t q = s_item;
     if (q >= total) break;
+    // order with lag G: P1(0..G-1) | [P1(j) P2(j-G)] for j = G..ns-1 | P2(ns-G..ns-1)
     bool is_p1;
     uint32_t j, r;
-    if (q < N1) {
-      is_p1 = true; j = 0; r = (uint32_t)q;
+    const uint32_t G = args.lag < ns ? args.lag : ns;
+    if (q < (uint64_t)G * N1) {
+      is_p1 = true; j = (uint32_t)(q / N1); r = (uint32_t)(q - (uint64_t)j * N1);
     } else {
-      const uint64_t q2 = q - N1;
+      const uint64_t q2 = q - (uint64_t)G * N1;
       const uint32_t pr = (uint32_t)(q2 / (N1 + N2));
       const uint32_t rr = (uint32_t)(q2 - (uint64_t)pr * (N1 + N2));
-      if (pr + 1 < ns) {
-        if (rr < N1) { is_p1 = true; j = pr + 1; r = rr; }
+      if (pr + G < ns) {
+        if (rr < N1) { is_p1 = true; j = pr + G; r = rr; }
         else { is_p1 = false; j = pr; r = rr - N1; }
       } else {
-        is_p1 = false; j = pr; r = rr;
+        // tail: the remaining pass-2 items, N2 per slab
+        const uint64_t q3 = q2 - (uint64_t)(ns - G) * (N1 + N2);
+        is_p1 = false; j = (ns - G) + (uint32_t)(q3 / N2); r = (uint32_t)(q3 % N2);
       }
     }
     const uint32_t loc = args.order[j];

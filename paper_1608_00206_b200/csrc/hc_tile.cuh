@@ -267,6 +267,7 @@ struct SlabArgs {
   uint32_t* ctr;       // [0] = work counter, [1 + j] = pass-1 tiles done in slab j
   const uint32_t* order;  // processing position j -> slab offset within the launch (cost-sorted)
   int debug_skip;      // timing experiments only (HC_DEBUG_SKIP): 1 = no pass 2, 2 = no pass 1
+  uint32_t lag;        // pass 2 of slab j is scheduled after pass 1 of slab j + lag (>= 1)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
