@@ -127,18 +127,32 @@ hc_status check_device() {
 }
 
 // ---- 8-axis tiles: single level (tile8_kernel) and two levels (prep + slab8_kernel) ----
+// persistent grid size for a T8 kernel: SMs x resident CTAs per SM
+template <class K>
+cudaError_t t8_grid(K kern, int& grid_max) {
+  if (grid_max) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T8Cfg<double>::SMEM);
+  if (e != cudaSuccess) return e;
+  int occ = 0, dev = 0, sms = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T8_NT, T8Cfg<double>::SMEM);
+  if (e != cudaSuccess) return e;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  grid_max = occ * sms;
+  return cudaSuccess;
+}
+
 template <class T>
 cudaError_t launch_tile8(const T* x, const T* y, T* z, int D, uint64_t slab0, uint64_t nslab, uint64_t nitems,
                          cudaStream_t st) {
   auto kern = tile8_kernel<T>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T8Cfg<T>::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static int grid_max = 0;
+  cudaError_t e = t8_grid(kern, grid_max);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)(nitems < (uint64_t)grid_max ? nitems : (uint64_t)grid_max);
   LaunchScope ls("tile", st);
-  kern<<<(unsigned)nitems, T8_NT, T8Cfg<T>::SMEM, st>>>(x, y, z, D, slab0, nslab);
+  kern<<<grid, T8_NT, T8Cfg<T>::SMEM, st>>>(x, y, z, D, slab0, nslab, nitems);
   return cudaGetLastError();
 }
 
@@ -146,20 +160,11 @@ template <class T, int M>
 cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st) {
   auto kern = slab8_kernel<T, M>;
   static int grid_max = 0;
-  if (!grid_max) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T8Cfg<T>::SMEM);
-    if (e != cudaSuccess) return e;
-    int occ = 0, dev = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T8_NT, T8Cfg<T>::SMEM);
-    if (e != cudaSuccess) return e;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (occ < 1) return cudaErrorInvalidConfiguration;
-    grid_max = occ * sms;
-  }
+  cudaError_t e = t8_grid(kern, grid_max);
+  if (e != cudaSuccess) return e;
   const uint64_t items = (uint64_t)a.nslab * (upow3(M) + upow3(8) / P2W);
   const unsigned grid = (unsigned)(items < (uint64_t)grid_max ? items : (uint64_t)grid_max);
-  cudaError_t e = cudaMemsetAsync(a.ctr, 0, sizeof(uint32_t) * (1 + (size_t)a.nslab), st);
+  e = cudaMemsetAsync(a.ctr, 0, sizeof(uint32_t) * (1 + (size_t)a.nslab), st);
   if (e != cudaSuccess) return e;
   {
     LaunchScope lp("prep", st);
@@ -430,12 +435,30 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
     static const int dbg = getenv("HC_DEBUG_SKIP") ? atoi(getenv("HC_DEBUG_SKIP")) : 0;
     static const int lag = getenv("HC_SLAB_LAG") ? atoi(getenv("HC_SLAB_LAG")) : 1;
     SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg, (uint32_t)(lag < 1 ? 1 : lag)};
+#ifdef HC_PHASE_PROF
+    {
+      unsigned long long zero[16] = {0};
+      cudaMemcpyToSymbolAsync(hc_phase, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
+    }
+#endif
     if (p->dtype == HC_INT64)
       e = launch_slab8<uint64_t>((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)z, (uint64_t*)p->xu,
                                  (uint64_t*)p->yu, g.M, a, st);
     else
       e = launch_slab8<double>((const double*)x, (const double*)y, (double*)z, (double*)p->xu, (double*)p->yu,
                                g.M, a, st);
+#ifdef HC_PHASE_PROF
+    {
+      unsigned long long h[16];
+      cudaMemcpyFromSymbolAsync(h, hc_phase, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      double tot = 0;
+      for (int i = 0; i < 7; ++i) tot += (double)h[i];
+      fprintf(stderr, "phase(Mclk/CTA-sum): select+wait %.0f pairloop %.0f inv+store %.0f p2 %.0f end %.0f "
+              "(tot %.0f) | F1 mbar wait %.0f\n", h[0] / 1e6, h[1] / 1e6, h[6] / 1e6, h[4] / 1e6, h[5] / 1e6,
+              tot / 1e6, h[7] / 1e6);
+    }
+#endif
   }
   return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
 }

@@ -6,16 +6,20 @@
 // pointwise product, inverse (c0, (c1-c0)-c2, c2) -- on the 8 tile axes and the M middle
 // axes; the paper's 4-way split (PAPER.md 166-177) on the k top axes (pair-sum).
 //
-// Tile (3^8 = 6561 outputs, 243 threads = (e_A in 3^2) x (e_B in 3^3), 27 accumulators per
-// thread over the C = 3 register axes).  Per top pair (i_T, j_T):
-//   * the raw input slices (256 values of x and of y; for the two-level engine already
-//     evaluated over the middle axes by prep_kernel) are prefetched two pairs ahead with
-//     cp.async into a 3-deep SMEM ring (no registers held, latency hidden);
-//   * 144 "line" threads (operand, e_A, b_lo) evaluate the A axes (sum of the rows
-//     consistent with e_A) and the B axes (8 -> 27 in registers) and write the stage P;
-//   * every thread loads its 8 + 8 base values from P and evaluates the C axes fused with
-//     the product into its accumulators (fwd_mul_acc).
-// Then the tile is interpolated (registers -> SMEM -> SMEM) and stored.
+// Tile axes (bit / trit b of the tile index, b = 0 fastest):
+//   C = {0,1,2}  register axes: 27 accumulators per thread
+//   B = {3,4,5}  evaluated by the F1 warps, in registers
+//   a1 = 6       evaluated by the F1 warps (one warp per evaluation point e_a1)
+//   a2 = 7       summed by the F2 threads while they load (e_a2 = 1: two rows)
+// CTA = 8 warps (2 CTAs/SM, 4 warps per SM sub-partition: 128 registers per thread).
+// In F2 and the inverse, thread u < 243 owns (e_a2, e_a1, e_B) = u / 81, u / 27 % 3, u % 27;
+// warps 5-7 also run F1 (warp 5 + e_s evaluates a1 at e_s).
+//
+// Shared-memory cost model (measured, profiles/r01_smem_microbench.txt, tools/microbench/
+// mb4.cu): loads 256 B/clk/SM (LDS.64 at odd or aligned-contiguous lane strides, LDS.128 at
+// a 10-element stride), stores 128 B/clk/SM.  The split above keeps stores low: per pair
+// and tile F1 stores 2 ops x 2 b_a2 x 81 e_S x 8 b_C = 2592 elements, F2 loads
+// 243 x (4/3) x 16 = 5184 (LDS.128), F1 loads 4 x 256 = 1024.
 #pragma once
 #include "hc_tile.cuh"
 
@@ -63,18 +67,44 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-constexpr int T8_NT = 243;        // threads per tile CTA
-constexpr int T8_NLINE = 72;      // F1 lines per operand: (e_A in 9) x (b_lo in 8)
-constexpr int T8_PSZ = 2 * T8_NLINE * 27;   // one stage: both operands, 27 values per line
-constexpr int T8_RAW = 512;       // one raw stage: x slice + y slice
-constexpr int T8_NRAW = 3;        // raw prefetch depth
+// 16-byte shared load of two consecutive elements
+__device__ __forceinline__ void lds2(const double* p, double& a, double& b) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void lds2(const uint64_t* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(smem_u32(p)));
+}
+
+// ---- layouts (element offsets) ------------------------------------------------------
+constexpr int T8_NW = 8;              // warps per tile CTA
+constexpr int T8_NT = 32 * T8_NW;     // 256 threads (243 tile units)
+constexpr int T8_F1W = 5;             // first of the three F1 warps
+// raw stage: op*RS_OP + b_a2*RS_H2 + b_a1*RS_H1 + b_B*8 + b_C, filled by 2 TMA copies of
+// 128 elements (the b_a2 halves of the natural slice) per operand; the pads put the F1
+// lanes (op, b_a2, b_C) on 32 distinct 8-byte bank slots (RS_H2 = 8, RS_OP = 16 mod 32)
+constexpr int RS_H1 = 64, RS_H2 = 136, RS_OP = 304, RS_SZ = 608;
+// raw ring depth: the slices stream from HBM (the middle-axes tables) or L2; ~10 pairs of
+// lead (~3 us) hide the loaded-HBM latency across item boundaries
+#ifndef HC_NRAW
+#define HC_NRAW 4
+#endif
+constexpr int T8_NRAW = HC_NRAW;
+// P stage (F1 output): op*PS_OP + b_a2*PS_A2 + e_S*PS_ROW + b_C, e_S = e_B + 27 e_a1.
+// PS_ROW = 10: the F2 lanes (consecutive e_S) read 16 B at a 80-B stride (conflict-free);
+// PS_A2 = 8 and PS_OP = 16 (mod 32): the F1 stores of one warp hit 32 distinct slots.
+constexpr int PS_ROW = 10, PS_A2 = 840, PS_OP = 1680, PS_SZ = 3360;
+// tile exchange buffer S (3^8) and the pass-2 buffer alias the two P stages
+constexpr int T8_PBUF = 2 * PS_SZ + 8;
+
 template <class T>
 struct T8Cfg {
-  static constexpr size_t SMEM = sizeof(T) * (size_t)(2 * T8_PSZ + T8_NRAW * T8_RAW);
-  static_assert(2 * T8_PSZ >= 6561, "tile exchange buffer aliases the two stages");
-  static_assert(2 * T8_PSZ >= P2Cfg<6>::SIZE, "pass-2 buffer aliases the two stages");
+  static constexpr int ALIAS = T8_PBUF > 6561 ? T8_PBUF : 6561;
+  static constexpr size_t SMEM = sizeof(T) * (size_t)(ALIAS + T8_NRAW * RS_SZ);
+  static_assert(P2Cfg<6>::SIZE <= ALIAS && P2Cfg<5>::SIZE <= ALIAS, "pass-2 buffer aliases the P stages");
 };
+
 
 // Prep kernel (two-level only): evaluate the M middle axes of every input slice once per
 // call, X_U[i_T][e_U][b_L] = sum_{b_U ~ e_U} x[i_T][b_U][b_L] (the forward transform over
@@ -97,22 +127,46 @@ __global__ void __launch_bounds__(256) prep_kernel(const T* __restrict__ x, cons
   *dst = acc;
 }
 
-// raw-slice staging: T8_NRAW stages, each filled by two TMA bulk copies (x slice, y slice)
-// and completed on its mbarrier.  seq counts fills over the CTA's lifetime (same value in
-// every thread) so the parity of each stage's barrier is known.
+// ---- optional phase instrumentation (-DHC_PHASE_PROF; development builds only) -------
+#ifdef HC_PHASE_PROF
+__device__ unsigned long long hc_phase[16];
+__device__ __forceinline__ long long* ph_sh() {
+  __shared__ long long s_ph[10];  // [0..7] phase sums, [8] thread-0 timestamp, [9] wait start
+  return s_ph;
+}
+#define PH_DECL do { if (threadIdx.x == 0) { for (int i_ = 0; i_ < 8; ++i_) ph_sh()[i_] = 0; ph_sh()[8] = clock64(); } } while (0)
+#define PH_MARK(i) do { if (threadIdx.x == 0) { long long t_ = clock64(); ph_sh()[i] += t_ - ph_sh()[8]; ph_sh()[8] = t_; } } while (0)
+#define PH_WAIT_BEGIN(c) long long phw_ = (c) ? clock64() : 0
+#define PH_WAIT_END(c) do { if (c) atomicAdd((unsigned long long*)&ph_sh()[7], (unsigned long long)(clock64() - phw_)); } while (0)
+#define PH_FLUSH do { if (threadIdx.x == 0) for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&hc_phase[i_], (unsigned long long)ph_sh()[i_]); } while (0)
+#else
+#define PH_DECL do { } while (0)
+#define PH_MARK(i) do { } while (0)
+#define PH_WAIT_BEGIN(c) do { } while (0)
+#define PH_WAIT_END(c) do { } while (0)
+#define PH_FLUSH do { } while (0)
+#endif
+
+// ---- raw-slice staging ring and the cross-item prefetcher -----------------------------
+// T8_NRAW stages; stage n is filled by 4 TMA copies (x and y, two 128-element halves each)
+// and completes on its mbarrier.  `done` counts fills consumed by F1 (advanced identically
+// in every thread); `seq` (thread 0) counts fills issued.  Fill n may be issued once fill
+// n - T8_NRAW has been read, i.e. seq - done < T8_NRAW at a point after a barrier.
 struct RawRing {
   uint64_t* bar;     // [T8_NRAW] in shared memory
-  uint32_t seq;      // fills issued so far
+  uint32_t seq;      // fills issued so far (thread 0)
   uint32_t done;     // fills consumed so far
 };
 template <class T>
 __device__ __forceinline__ void t8_issue(RawRing& rr, const T* sx, const T* sy, T* R, uint64_t pol) {
   const uint32_t st = rr.seq % T8_NRAW;
-  if (threadIdx.x == 0) {
-    mbar_arrive_tx(&rr.bar[st], 2 * 256 * sizeof(T));
-    tma_load_1d(R + st * T8_RAW, sx, 256 * sizeof(T), &rr.bar[st], pol);
-    tma_load_1d(R + st * T8_RAW + 256, sy, 256 * sizeof(T), &rr.bar[st], pol);
-  }
+  uint64_t* bar = &rr.bar[st];
+  T* dst = R + st * RS_SZ;
+  mbar_arrive_tx(bar, 2 * 256 * sizeof(T));
+  tma_load_1d(dst, sx, 128 * sizeof(T), bar, pol);
+  tma_load_1d(dst + RS_H2, sx + 128, 128 * sizeof(T), bar, pol);
+  tma_load_1d(dst + RS_OP, sy, 128 * sizeof(T), bar, pol);
+  tma_load_1d(dst + RS_OP + RS_H2, sy + 128, 128 * sizeof(T), bar, pol);
   ++rr.seq;
 }
 __device__ __forceinline__ uint32_t t8_wait(RawRing& rr) {
@@ -122,150 +176,268 @@ __device__ __forceinline__ uint32_t t8_wait(RawRing& rr) {
   return st;
 }
 
-// stage F1 of one pair: raw slices R -> P (line threads tid < 144)
+// Stage F1 of one pair (warps T8_F1W + e_s): lane (op, b_a2, b_C) evaluates the a1 axis at
+// e_s and the three B axes (PAPER.md 186-189 per axis), and stores the 27 values e_B.
 template <class T>
-__device__ __forceinline__ void t8_f1(const T* R, T* P, int tid, uint32_t lbase, uint32_t lfree) {
-  if (tid >= 2 * T8_NLINE) return;
-  const int op = tid / T8_NLINE, rr = tid - op * T8_NLINE;
-  const int blo = rr & 7;
-  const T* src = R + op * 256 + blo;
+__device__ __forceinline__ void t8_f1(const T* R, T* P, int es, int lane) {
+  const int op = lane >> 4, ba2 = (lane >> 3) & 1, bc = lane & 7;
+  const T* src = R + op * RS_OP + ba2 * RS_H2 + bc;
   T in[8];
+  if (es == 0) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) in[j] = T(0);
-  uint32_t sa = 0;
-  do {  // forward over the A axes: rows b_A consistent with e_A
-    const T* row = src + (lbase | sa) * 64;
+    for (int j = 0; j < 8; ++j) in[j] = src[8 * j];
+  } else if (es == 2) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) in[j] = Ar<T>::add(in[j], row[8 * j]);
-    sa = (sa - lfree) & lfree;
-  } while (sa != 0);
+    for (int j = 0; j < 8; ++j) in[j] = src[RS_H1 + 8 * j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) in[j] = Ar<T>::add(src[8 * j], src[RS_H1 + 8 * j]);
+  }
   T out[27];
-  fwd_reg<3, T>(in, out);  // forward over the B axes
-  T* dst = P + op * (T8_NLINE * 27) + rr * 27;
+  fwd_reg<3, T>(in, out);
+  T* dst = P + op * PS_OP + ba2 * PS_A2 + (27 * es) * PS_ROW + bc;
 #pragma unroll
-  for (int e = 0; e < 27; ++e) dst[e] = out[e];
+  for (int e = 0; e < 27; ++e) dst[e * PS_ROW] = out[e];
 }
 
-// One pass-1 tile.  sx0/sy0 + iT*stride are the raw x / y slices of pair (iT, jT).
-template <class T, bool FINAL>
-__device__ __forceinline__ void tile8(const T* __restrict__ sx0, const T* __restrict__ sy0, uint64_t stride,
-                                      T* __restrict__ zt, int k, uint64_t tT, T* sm, RawRing& rr,
-                                      uint64_t pol_in, uint64_t pol_out) {
-  T* P = sm;                          // [2][T8_PSZ]
-  T* R = sm + 2 * T8_PSZ;             // [T8_NRAW][T8_RAW]
-  T* S = sm;                          // [9][27][27] after the pair loop (aliases P)
-  const int tid = threadIdx.x;
-  const int eA = tid / 27, eB = tid - eA * 27;
-
-  // this thread's F1 line (tid < 144): e_A of the line -> rows consistent with it
-  uint32_t lbase = 0, lfree = 0;
-  {
-    int t = (tid % T8_NLINE) >> 3;
+// Stage F2 of one pair: thread (e_a2, e_S) loads its 8 + 8 base values (summing the two
+// b_a2 rows when e_a2 = 1) and runs the C-axes forward fused with the product.
+template <class T>
+__device__ __forceinline__ void t8_f2(const T* P, int ea2, int eS, T* acc) {
+  const T* px = P + eS * PS_ROW;
+  T xt[8], yt[8];
+  if (ea2 != 1) {
+    const T* a = px + (ea2 >> 1) * PS_A2;
 #pragma unroll
-    for (int aa = 0; aa < 2; ++aa) {
-      const int d = t % 3;
-      t /= 3;
-      if (d == 2) lbase |= 1u << aa;
-      else if (d == 1) lfree |= 1u << aa;
+    for (int j = 0; j < 8; j += 2) {
+      lds2(a + j, xt[j], xt[j + 1]);
+      lds2(a + PS_OP + j, yt[j], yt[j + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      T u0, u1, v0, v1;
+      lds2(px + j, xt[j], xt[j + 1]);
+      lds2(px + PS_A2 + j, u0, u1);
+      lds2(px + PS_OP + j, yt[j], yt[j + 1]);
+      lds2(px + PS_OP + PS_A2 + j, v0, v1);
+      xt[j] = Ar<T>::add(xt[j], u0);
+      xt[j + 1] = Ar<T>::add(xt[j + 1], u1);
+      yt[j] = Ar<T>::add(yt[j], v0);
+      yt[j + 1] = Ar<T>::add(yt[j + 1], v1);
     }
   }
-  uint32_t base, freeb;
-  trit_split(tT, k, base, freeb);
-  const int npairs = 1 << __popc(freeb);
+  fwd_mul_acc<3, T>(xt, yt, acc);
+}
 
-  // pair p: s_p = p-th subset of freeb (ascending), i_T = base|s_p, j_T = base|(freeb & ~s_p)
-  uint32_t s_pf = 0;  // subset of the next pair to prefetch
-  int npf = 0;        // pairs prefetched so far
-  auto prefetch_next = [&]() {
-    if (npf < npairs) {
-      const uint64_t iT = base | s_pf, jT = base | (freeb & ~s_pf);
-      t8_issue<T>(rr, sx0 + iT * stride, sy0 + jT * stride, R, pol_in);
-      s_pf = (s_pf - freeb) & freeb;
-      ++npf;
+// Prefetch cursor (shared memory, thread 0 only) over the pairs of the pass-1 items in the
+// order the CTA will consume them.  Pair p of an item has subset s_p of freeb (ascending
+// subsets, PAPER.md 173-177 direct split): i_T = base | s_p, j_T = base | (freeb & ~s_p).
+struct Prefetch {
+  const void* sx0;
+  const void* sy0;
+  uint64_t stride;
+  uint32_t base, freeb, s;
+  int left;        // pairs of the cursor item not yet issued
+  uint32_t pos;    // position of the cursor item in the CTA's item sequence
+};
+
+// Fill the ring (thread 0).  next(pf) advances the cursor to the next pass-1 item the CTA
+// will run (setting sx0, sy0, stride, base, freeb, s = 0, left) or returns false.
+template <class T, class Next>
+__device__ __forceinline__ void pf_pump(Prefetch& pf, RawRing& rr, T* R, uint64_t pol, Next&& next) {
+  bool fenced = false;
+  while (rr.seq - rr.done < (uint32_t)T8_NRAW) {
+    if (pf.left == 0 && !next(pf)) return;
+    if (!fenced) {  // the stage's previous contents were read through the generic proxy
+      fence_proxy_async();
+      fenced = true;
     }
+    const uint64_t iT = pf.base | pf.s, jT = pf.base | (pf.freeb & ~pf.s);
+    t8_issue<T>(rr, (const T*)pf.sx0 + iT * pf.stride, (const T*)pf.sy0 + jT * pf.stride, R, pol);
+    pf.s = (pf.s - pf.freeb) & pf.freeb;
+    --pf.left;
+  }
+}
+
+// One pass-1 tile with `npairs` top pairs whose raw slices arrive, in order, through the
+// ring (issued by the pump).  Computes the tile's 3^8 values (final for the single-level
+// engine, evaluation domain of the middle axes for the slab engine) and stores them to zt.
+template <class T, bool FINAL, class Pump, class Mid>
+__device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, RawRing& rr, uint64_t pol_out,
+                                      Pump&& pump, Mid&& mid) {
+  T* P = sm;                          // [2][PS_SZ]
+  T* R = sm + T8Cfg<T>::ALIAS;        // [T8_NRAW][RS_SZ]
+  T* S = sm;                          // [9][27][27] after the pair loop (aliases P)
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const bool unit = tid < 243;                     // F2 / inverse unit (e_a2, e_S)
+  const int ea2 = tid / 81, eS = tid - 81 * ea2;   // e_S = e_B + 27 e_a1
+  // F1: warps T8_F1W + e_s evaluate a1 at e_s (the other warps only advance the ring count)
+  auto f1 = [&](int, T* Pd) {
+    if (w >= T8_F1W) t8_f1<T>(R + t8_wait(rr) * RS_SZ, Pd, w - T8_F1W, lane);
+    else ++rr.done;
   };
 
-  __syncthreads();      // previous users of sm (and of the raw stages) are done
-  prefetch_next();      // pair 0
-  prefetch_next();      // pair 1
-  t8_f1<T>(R + t8_wait(rr) * T8_RAW, P, tid, lbase, lfree);
+  if (tid == 0) pump();
+  f1(0, P);
   __syncthreads();
 
   T acc[27];
 #pragma unroll
   for (int i = 0; i < 27; ++i) acc[i] = T(0);
   for (int p = 0; p < npairs; ++p) {
-    prefetch_next();  // pair p + 2 (its stage was last read by F1(p - 1), before a barrier)
-    {
-      // base values of (e_A, e_B): one line per b_lo, then C-axes forward fused with product
-      const T* fx = P + (p & 1) * T8_PSZ;
-      const T* fy = fx + T8_NLINE * 27;
-      T xt[8], yt[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int idx = (eA * 8 + j) * 27 + eB;
-        xt[j] = fx[idx];
-        yt[j] = fy[idx];
-      }
-      fwd_mul_acc<3, T>(xt, yt, acc);
-    }
-    if (p + 1 < npairs) t8_f1<T>(R + t8_wait(rr) * T8_RAW, P + ((p + 1) & 1) * T8_PSZ, tid, lbase, lfree);
+    if (tid == 0) pump();  // refill the stage F1(p) released
+    if (p + 1 < npairs) f1(p + 1, P + ((p + 1) & 1) * PS_SZ);
+    if (unit) t8_f2<T>(P + (p & 1) * PS_SZ, ea2, eS, acc);
     __syncthreads();
   }
+  if (tid == 0) {
+    pump();
+    mid();  // no global stores of this CTA are in flight here: cheap place for a release
+  }
+  PH_MARK(1);
 
-  // a4: inverse on the C register axes, then B (SMEM exchange), then A + store (a6)
-  inv_reg<3, T>(acc);
+  // a4: inverse on the C register axes, then B (SMEM exchange), then A + store (a6).
+  // Unit u = (e_A, e_B) with e_A = e_a1 + 3 e_a2, so S[e_A][e_B][k_C] = S[27 u + k_C].
+  if (unit) {
+    inv_reg<3, T>(acc);
 #pragma unroll
-  for (int i = 0; i < 27; ++i) S[tid * 27 + i] = acc[i];
-  __syncthreads();
-  {
-    const int aa = tid / 27, tl = tid - aa * 27;
-    T v[27];
-#pragma unroll
-    for (int e = 0; e < 27; ++e) v[e] = S[(aa * 27 + e) * 27 + tl];
-    inv_reg<3, T>(v);
-#pragma unroll
-    for (int e = 0; e < 27; ++e) S[(aa * 27 + e) * 27 + tl] = v[e];
+    for (int i = 0; i < 27; ++i) S[tid * 27 + i] = acc[i];
   }
   __syncthreads();
-  for (int w = tid; w < 729; w += T8_NT) {
-    T v[9];
+  if (unit) {  // unit (e_A, k_C): interpolate the B axes
+    const int a = tid / 27, c = tid - 27 * a;
+    T v[27];
 #pragma unroll
-    for (int e = 0; e < 9; ++e) v[e] = S[e * 729 + w];
-    inv_reg<2, T>(v);
+    for (int e = 0; e < 27; ++e) v[e] = S[a * 729 + e * 27 + c];
+    inv_reg<3, T>(v);
 #pragma unroll
-    for (int e = 0; e < 9; ++e) {
-      if constexpr (FINAL) st_cs(zt + e * 729 + w, v[e]);
-      else st_hint(zt + e * 729 + w, v[e], pol_out);
+    for (int e = 0; e < 27; ++e) S[a * 729 + e * 27 + c] = v[e];
+  }
+  __syncthreads();
+  if (unit) {  // columns (k_B, k_C), three rounds of 243: interpolate the A axes, store
+#pragma unroll 1
+    for (int r = 0; r < 3; ++r) {
+      const int col = r * 243 + tid;
+      T v[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) v[e] = S[e * 729 + col];
+      inv_reg<2, T>(v);
+#pragma unroll
+      for (int e = 0; e < 9; ++e) {
+        if constexpr (FINAL) st_cs(zt + e * 729 + col, v[e]);
+        else st_hint(zt + e * 729 + col, v[e], pol_out);
+      }
     }
   }
 }
 
-// Single-level kernel for 8-axis tiles (8 <= D <= 12, batched D >= 8): work item w covers
-// batch b = w / nslab, top index t_T = slab0 + w % nslab, writes z[w * 6561 ...].
-template <class T>
-__global__ void __launch_bounds__(T8_NT, 2)
-tile8_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z, int D, uint64_t slab0,
-             uint64_t nslab) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* sm = reinterpret_cast<T*>(smem_raw);
-  __shared__ __align__(8) uint64_t raw_bar[T8_NRAW];
+__device__ __forceinline__ void ring_init(uint64_t* bars) {
   if (threadIdx.x == 0) {
-    for (int i = 0; i < T8_NRAW; ++i) mbar_init(&raw_bar[i], 1);
+    for (int i = 0; i < T8_NRAW; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+}
+
+// Single-level persistent kernel for 8-axis tiles (8 <= D <= 12, batched D >= 8): item w
+// (w = blockIdx.x, + gridDim.x, ...) covers batch b = w / nslab, top index
+// t_T = slab0 + w % nslab, and writes z[w * 6561 ...].  The prefetcher walks the same
+// static item sequence, so slices of the next tiles load while this one computes.
+template <class T>
+__global__ void __launch_bounds__(T8_NT, 2)
+tile8_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z, int D, uint64_t slab0,
+             uint64_t nslab, uint64_t nitems) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  __shared__ __align__(8) uint64_t raw_bar[T8_NRAW];
+  __shared__ Prefetch pf;
+  ring_init(raw_bar);
   RawRing rr{raw_bar, 0, 0};
-  const uint64_t w = blockIdx.x;
-  const uint64_t b = w / nslab;
-  const uint64_t tT = slab0 + (w - b * nslab);
-  tile8<T, true>(x + (b << D), y + (b << D), 256, z + w * 6561ull, D - 8, tT, sm, rr, policy_evict_last(), 0);
+  const int k = D - 8;
+  const uint64_t pol_in = policy_evict_last();
+  if (threadIdx.x == 0) {
+    pf.left = 0;
+    pf.pos = 0xffffffffu;  // next() moves to position 0
+  }
+  T* R = sm + T8Cfg<T>::ALIAS;
+  auto next = [&](Prefetch& c) -> bool {
+    const uint32_t np = c.pos + 1;
+    const uint64_t w = blockIdx.x + (uint64_t)np * gridDim.x;
+    if (w >= nitems) return false;
+    const uint64_t b = w / nslab;
+    uint32_t base, freeb;
+    trit_split(slab0 + (w - b * nslab), k, base, freeb);
+    c.pos = np;
+    c.sx0 = x + (b << D);
+    c.sy0 = y + (b << D);
+    c.stride = 256;
+    c.base = base;
+    c.freeb = freeb;
+    c.s = 0;
+    c.left = 1 << __popc(freeb);
+    return true;
+  };
+  auto pump = [&]() { pf_pump<T>(pf, rr, R, pol_in, next); };
+  for (uint64_t w = blockIdx.x; w < nitems; w += gridDim.x) {
+    const uint64_t b = w / nslab;
+    uint32_t base, freeb;
+    trit_split(slab0 + (w - b * nslab), k, base, freeb);
+    tile8<T, true>(1 << __popc(freeb), z + w * 6561ull, sm, rr, 0, pump, [] {});
+    __syncthreads();  // S (aliases P) is free before the next tile's F1
+  }
 }
 
 // Two-level persistent kernel: pass-1 items (slab j, e_U) and pass-2 items (slab j, 9
 // columns) from one work counter in the order P1(0) P1(1) P2(0) P1(2) P2(1) ...; slabs in
-// cost order (args.order).  See hc_tile.cuh (SlabArgs, p2_item) for the pass-2 side and the
-// deadlock argument.
+// cost order (args.order).  Each CTA holds T8_QN claimed items ("slots"), decoded by
+// thread 0 when the claim returns.  Selection: a pass-2 item whose slab is complete
+// (lowest claim first), else the lowest pass-1 item, else wait for the lowest pass-2 item.
+// Pass-1 items therefore run in claim order, which is the order the prefetcher issues
+// their slices.  Deadlock freedom: pass-1 items wait for nothing; a pass-2 item waits only
+// for pass-1 items of its slab, all claimed earlier.  The earliest unfinished claim is
+// either a pass-1 item -- its CTA never blocks while holding it (a ready pass-2 item or a
+// pass-1 item is always preferred to waiting) -- or a pass-2 item whose dependencies are
+// done, so it progresses (given a co-resident grid: grid <= SMs x occupancy).  A CTA
+// signals a finished pass-1 tile one item later (its stores have drained by then, so the
+// release fence is cheap), and always before it starts to wait.
+struct ItemDec {
+  bool p1;
+  uint32_t j, r;
+};
+__device__ __forceinline__ ItemDec decode_item(uint32_t q, uint32_t ns, uint32_t N1, uint32_t N2, uint32_t lag) {
+  // order with lag G: P1(0..G-1) | [P1(j) P2(j-G)] for j = G..ns-1 | P2(ns-G..ns-1)
+  ItemDec d;
+  const uint32_t G = lag < ns ? lag : ns;
+  if (q < G * N1) {
+    d.p1 = true; d.j = q / N1; d.r = q - d.j * N1;
+  } else {
+    const uint32_t q2 = q - G * N1;
+    const uint32_t pr = q2 / (N1 + N2);
+    const uint32_t rr = q2 - pr * (N1 + N2);
+    if (pr + G < ns) {
+      if (rr < N1) { d.p1 = true; d.j = pr + G; d.r = rr; }
+      else { d.p1 = false; d.j = pr; d.r = rr - N1; }
+    } else {
+      const uint32_t q3 = q2 - (ns - G) * (N1 + N2);
+      d.p1 = false; d.j = (ns - G) + q3 / N2; d.r = q3 % N2;
+    }
+  }
+  return d;
+}
+
+#ifndef HC_QN
+#define HC_QN 3
+#endif
+constexpr int T8_QN = HC_QN;  // claimed items held per CTA
+constexpr uint32_t T8_EXH = 0xffffffffu;
+
+struct Slot {
+  uint32_t q;            // claim index, T8_EXH = past the end
+  uint32_t p1, j, r, loc;
+  uint32_t base, freeb;  // pass 1: trit split of the slab's top index
+};
+
 template <class T, int M>
 __global__ void __launch_bounds__(T8_NT, 2)
 slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__ z, SlabArgs args) {
@@ -274,73 +446,174 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   constexpr uint64_t SLAB = upow3(M + 8);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  __shared__ uint32_t s_item;
+  __shared__ Slot s_slot[T8_QN];
+  __shared__ int s_sel;
   __shared__ __align__(8) uint64_t raw_bar[T8_NRAW];
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < T8_NRAW; ++i) mbar_init(&raw_bar[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
+  __shared__ Prefetch pf;
+  ring_init(raw_bar);
   RawRing rr{raw_bar, 0, 0};
   const uint32_t ns = args.nslab;
-  const uint64_t total = (uint64_t)ns * (N1 + N2);
+  const uint32_t total = ns * (N1 + N2);
+  const uint32_t lag = args.lag;
   const uint64_t pol_in = policy_evict_first();   // middle-axes tables are streamed
   const uint64_t pol_keep = policy_evict_last();  // pass-1 tiles wait in L2 for pass 2
   const uint64_t stride = upow3(M) * 256;
-  // claim one item ahead so the atomic's latency overlaps the current item (the claim order
-  // -- and with it the deadlock argument -- is unchanged)
-  uint32_t nq = threadIdx.x == 0 ? atomicAdd(args.ctr, 1u) : 0u;
-  while (true) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      s_item = nq;
-      nq = atomicAdd(args.ctr, 1u);
+  const bool skip1 = args.debug_skip == 2, skip2 = args.debug_skip == 1;
+  T* R = sm + T8Cfg<T>::ALIAS;
+  uint32_t* done_ctr = args.ctr + 1;
+
+  // thread-0 helpers ------------------------------------------------------------------
+  auto decode = [&](uint32_t q, Slot& o) {
+    if (q >= total) { o.q = T8_EXH; return; }
+    const ItemDec d = decode_item(q, ns, N1, N2, lag);
+    o.q = q; o.p1 = d.p1; o.j = d.j; o.r = d.r;
+    o.loc = args.order[d.j];
+    if (d.p1) trit_split(args.slab0 + o.loc, args.k, o.base, o.freeb);
+  };
+  // prefetch cursor: pass-1 slots in claim order (pf.pos = claim index of the cursor item)
+  auto next = [&](Prefetch& c) -> bool {
+    if (skip1) return false;
+    int best = -1;
+    for (int i = 0; i < T8_QN; ++i) {
+      const Slot& o = s_slot[i];
+      if (o.q == T8_EXH || !o.p1 || (c.pos != T8_EXH && o.q <= c.pos)) continue;
+      if (best < 0 || o.q < s_slot[best].q) best = i;
     }
-    __syncthreads();
-    const uint64_t q = s_item;
-    if (q >= total) break;
-    // order with lag G: P1(0..G-1) | [P1(j) P2(j-G)] for j = G..ns-1 | P2(ns-G..ns-1)
-    bool is_p1;
-    uint32_t j, r;
-    const uint32_t G = args.lag < ns ? args.lag : ns;
-    if (q < (uint64_t)G * N1) {
-      is_p1 = true; j = (uint32_t)(q / N1); r = (uint32_t)(q - (uint64_t)j * N1);
-    } else {
-      const uint64_t q2 = q - (uint64_t)G * N1;
-      const uint32_t pr = (uint32_t)(q2 / (N1 + N2));
-      const uint32_t rr = (uint32_t)(q2 - (uint64_t)pr * (N1 + N2));
-      if (pr + G < ns) {
-        if (rr < N1) { is_p1 = true; j = pr + G; r = rr; }
-        else { is_p1 = false; j = pr; r = rr - N1; }
-      } else {
-        // tail: the remaining pass-2 items, N2 per slab
-        const uint64_t q3 = q2 - (uint64_t)(ns - G) * (N1 + N2);
-        is_p1 = false; j = (ns - G) + (uint32_t)(q3 / N2); r = (uint32_t)(q3 % N2);
-      }
+    if (best < 0) return false;
+    const Slot& o = s_slot[best];
+    c.pos = o.q;
+    c.sx0 = xu + (uint64_t)o.r * 256;
+    c.sy0 = yu + (uint64_t)o.r * 256;
+    c.stride = stride;
+    c.base = o.base;
+    c.freeb = o.freeb;
+    c.s = 0;
+    c.left = 1 << __popc(o.freeb);
+    return true;
+  };
+  auto pump = [&]() { pf_pump<T>(pf, rr, R, pol_in, next); };
+  uint32_t pend = T8_EXH;  // thread 0: slab position of a finished, not yet signalled tile
+  // Completion of a pass-1 tile is published with a gpu-scope fence (cumulative over the
+  // CTA's stores, which precede it through a CTA barrier) and an atomic increment.  Called
+  // where thread 0 has no global stores in flight (mid item, before a wait, at exit).
+  auto signal = [&]() {
+    if (pend != T8_EXH) {
+      __threadfence();
+      atomicAdd(done_ctr + pend, 1u);
+      pend = T8_EXH;
     }
-    const uint32_t loc = args.order[j];
-    T* zs = z + (uint64_t)loc * SLAB;
-    if (is_p1) {
-      if (args.debug_skip == 2) {
-        if (threadIdx.x == 0) atomicAdd(args.ctr + 1 + j, 1u);
-        continue;
-      }
-      tile8<T, false>(xu + (uint64_t)r * 256, yu + (uint64_t)r * 256, stride, zs + (uint64_t)r * 6561ull, args.k,
-                      args.slab0 + loc, sm, rr, pol_in, pol_keep);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(args.ctr + 1 + j, 1u);
-      }
-    } else {
-      if (args.debug_skip == 1) continue;
-      if (threadIdx.x == 0) {
-        while (ld_acquire(args.ctr + 1 + j) < N1) __nanosleep(256);
-      }
-      __syncthreads();
-      p2_item<T, M, 8>(zs, r, sm, T8_NT);
-    }
+  };
+
+  if (threadIdx.x == 0) {
+    uint32_t c[T8_QN];
+    for (int i = 0; i < T8_QN; ++i) c[i] = atomicAdd(args.ctr, 1u);
+    for (int i = 0; i < T8_QN; ++i) decode(c[i], s_slot[i]);
+    pf.left = 0;
+    pf.pos = T8_EXH;
   }
+  // thread 0, kept across one item so that global-memory latencies overlap the item:
+  uint32_t cv[T8_QN];          // slab-completion counters of the pass-2 slots (loaded at item start)
+  uint32_t cmask = 0;          // slots whose cv[] is valid
+  int pslot = -1;              // slot whose claim is being decoded: claim index pq, order value ov
+  uint32_t pq = 0, pov = 0;
+  ItemDec pd{};
+  PH_DECL;
+  while (true) {
+    if (threadIdx.x == 0) {
+      auto finish_pending = [&]() {  // complete the claim decoded one item ago
+        Slot& o = s_slot[pslot];
+        o.q = pq; o.p1 = pd.p1; o.j = pd.j; o.r = pd.r; o.loc = pov;
+        if (pd.p1) trit_split(args.slab0 + pov, args.k, o.base, o.freeb);
+        pslot = -1;
+      };
+      int sel, p2w;
+      for (int pass = 0;; ++pass) {
+        int p2r = -1, p1 = -1;
+        p2w = -1;
+        for (int i = 0; i < T8_QN; ++i) {
+          const Slot& o = s_slot[i];
+          if (i == pslot || o.q == T8_EXH) continue;
+          if (o.p1) {
+            if (p1 < 0 || o.q < s_slot[p1].q) p1 = i;
+          } else if (skip2 || (((cmask >> i) & 1) && cv[i] >= N1)) {
+            if (p2r < 0 || o.q < s_slot[p2r].q) p2r = i;
+          } else if (p2w < 0 || o.q < s_slot[p2w].q) {
+            p2w = i;
+          }
+        }
+        sel = p2r >= 0 ? p2r : (p1 >= 0 ? p1 : p2w);
+        // before waiting (or leaving), the pending claim must be visible: it may be the
+        // pass-1 item everybody waits for
+        if ((sel < 0 || sel == p2w) && pslot >= 0 && pass == 0) {
+          finish_pending();
+          continue;
+        }
+        break;
+      }
+      if (sel >= 0 && sel == p2w) {  // nothing else to do: signal, then wait for the slab
+        signal();
+        pump();
+        const uint32_t j = s_slot[sel].j;
+        while (ld_relaxed(done_ctr + j) < N1) __nanosleep(64);
+      }
+      if (sel < 0) signal();
+      s_sel = sel;
+    }
+    __syncthreads();
+    const int sel = s_sel;
+    if (sel < 0) break;
+    const Slot it = s_slot[sel];
+    uint32_t claim = 0;
+    if (threadIdx.x == 0) {
+      claim = atomicAdd(args.ctr, 1u);  // refills slot `sel` after this item
+      cmask = 0;                         // snapshot the other pass-2 slots' slabs (used next time)
+      for (int i = 0; i < T8_QN; ++i) {
+        const Slot& o = s_slot[i];
+        if (i != sel && i != pslot && o.q != T8_EXH && !o.p1) {
+          cv[i] = ld_relaxed(done_ctr + o.j);  // non-blocking; compared at the next selection
+          cmask |= 1u << i;
+        }
+      }
+    }
+    PH_MARK(0);
+    T* zs = z + (uint64_t)it.loc * SLAB;
+    if (it.p1) {
+      if (skip1) {
+        if (threadIdx.x == 0) atomicAdd(done_ctr + it.j, 1u);
+      } else {
+        tile8<T, false>(1 << __popc(it.freeb), zs + (uint64_t)it.r * 6561ull, sm, rr, pol_keep, pump, signal);
+        PH_MARK(6);
+      }
+    } else if (!skip2) {
+      // the slab's tiles are complete (a relaxed read of its counter saw N1, then the CTA
+      // barrier): the reads below are ordered after it by that control dependency and the
+      // barrier, and go to L2 (.cg), where the producers' fenced stores already are
+      if (threadIdx.x == 0) pump();
+      p2_item<T, M, 8>(zs, it.r, sm, threadIdx.x < 243 ? (int)threadIdx.x : -1, signal);
+      PH_MARK(4);
+    }
+    __syncthreads();  // the item's smem is free
+    if (threadIdx.x == 0) {
+      if (it.p1 && !skip1) pend = it.j;  // published during the next item (or before a wait)
+      if (pslot >= 0) {                  // finish the claim decoded one item ago
+        Slot& o = s_slot[pslot];
+        o.q = pq; o.p1 = pd.p1; o.j = pd.j; o.r = pd.r; o.loc = pov;
+        if (pd.p1) trit_split(args.slab0 + pov, args.k, o.base, o.freeb);
+        pslot = -1;
+      }
+      // start decoding this item's replacement: the order[] load completes during the next item
+      if (claim >= total) {
+        s_slot[sel].q = T8_EXH;
+      } else {
+        pslot = sel;
+        pq = claim;
+        pd = decode_item(claim, ns, N1, N2, lag);
+        pov = args.order[pd.j];
+      }
+    }
+    PH_MARK(5);
+  }
+  PH_FLUSH;
 }
 
 }  // namespace hc

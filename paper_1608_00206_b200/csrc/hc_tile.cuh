@@ -275,6 +275,11 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 template <class T> __device__ __forceinline__ T ld_cg(const T* p);
 template <> __device__ __forceinline__ double ld_cg<double>(const double* p) {
   double v;
@@ -298,34 +303,37 @@ struct P2Cfg {
   static constexpr int P2S = NLO * P2W + ((9 - NLO * P2W) % 16 + 16) % 16;
   static constexpr int SIZE = NHI * P2S;
 };
-template <class T, int M, int L>
-__device__ __forceinline__ void p2_item(T* __restrict__ zs, uint32_t c, T* sm, int nthreads) {
+template <class T, int M, int L, class Mid>
+__device__ __forceinline__ void p2_item(T* __restrict__ zs, uint32_t c, T* sm, int task, Mid&& mid) {
+  // task in [0, 243) or -1 (idle lane); 243 = 3^5 task slots per round
   using Q = P2Cfg<M>;
   constexpr int LO = Q::LO, HI = Q::HI, NLO = Q::NLO, NHI = Q::NHI, P2S = Q::P2S;
   constexpr uint64_t ROW = upow3(L);
-  const int tid = threadIdx.x;
   const uint64_t col0 = (uint64_t)c * P2W;
-  // round 1: thread (e_hi, pos) loads its 3^LO column entries, interpolates over LO axes
-  for (int w = tid; w < NHI * P2W; w += nthreads) {
-    const int eh = w / P2W, pos = w - eh * P2W;
-    T v[NLO];
+  // round 1: task (e_hi, pos) loads its 3^LO column entries, interpolates over LO axes
+  if (task >= 0)
+    for (int w = task; w < NHI * P2W; w += 243) {
+      const int eh = w / P2W, pos = w - eh * P2W;
+      T v[NLO];
 #pragma unroll
-    for (int e = 0; e < NLO; ++e) v[e] = ld_cg(zs + (uint64_t)(eh * NLO + e) * ROW + col0 + pos);
-    inv_reg<LO, T>(v);
+      for (int e = 0; e < NLO; ++e) v[e] = ld_cg(zs + (uint64_t)(eh * NLO + e) * ROW + col0 + pos);
+      inv_reg<LO, T>(v);
 #pragma unroll
-    for (int e = 0; e < NLO; ++e) sm[eh * P2S + e * P2W + pos] = v[e];
-  }
+      for (int e = 0; e < NLO; ++e) sm[eh * P2S + e * P2W + pos] = v[e];
+    }
   __syncthreads();
-  // round 2: thread (e_lo, pos) interpolates over HI axes and stores the final values
-  for (int w = tid; w < NLO * P2W; w += nthreads) {
-    const int el = w / P2W, pos = w - el * P2W;
-    T v[NHI];
+  if (threadIdx.x == 0) mid();  // between the loads and the stores (see slab8_kernel)
+  // round 2: task (e_lo, pos) interpolates over HI axes and stores the final values
+  if (task >= 0)
+    for (int w = task; w < NLO * P2W; w += 243) {
+      const int el = w / P2W, pos = w - el * P2W;
+      T v[NHI];
 #pragma unroll
-    for (int e = 0; e < NHI; ++e) v[e] = sm[e * P2S + el * P2W + pos];
-    inv_reg<HI, T>(v);
+      for (int e = 0; e < NHI; ++e) v[e] = sm[e * P2S + el * P2W + pos];
+      inv_reg<HI, T>(v);
 #pragma unroll
-    for (int e = 0; e < NHI; ++e) st_cs(zs + (uint64_t)(e * NLO + el) * ROW + col0 + pos, v[e]);
-  }
+      for (int e = 0; e < NHI; ++e) st_cs(zs + (uint64_t)(e * NLO + el) * ROW + col0 + pos, v[e]);
+    }
 }
 
 }  // namespace hc

@@ -10,7 +10,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhc.so")
+LIB_PATH = os.environ.get("HC_LIB") or os.path.join(_HERE, "libhc.so")  # HC_LIB: development variants
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "hc.h")
 
 if not os.path.exists(LIB_PATH):

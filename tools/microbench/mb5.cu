@@ -1,0 +1,72 @@
+// Pair-loop throughput probe: runs the slab engine's F1 / F2 stages (hc_slab.cuh) on
+// SMEM-resident synthetic data, no TMA and no global traffic, and reports clk per pair
+// iteration per SM for: both stages + barrier, F2 only, F1 only, both without barrier.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../../paper_1608_00206_b200/csrc -o mb5 mb5.cu
+#include <cstdio>
+#include "hc_slab.cuh"
+
+using namespace hc;
+
+template <int MODE>
+__global__ void __launch_bounds__(T8_NT, 2) k_pairs(int iters, double* sink) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sm = reinterpret_cast<double*>(smem_raw);
+  double* P = sm;
+  double* R = sm + T8Cfg<double>::ALIAS;
+  for (int i = threadIdx.x; i < T8Cfg<double>::ALIAS + T8_NRAW * RS_SZ; i += T8_NT) sm[i] = 1e-3 * (i % 97);
+  __syncthreads();
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const bool unit = tid < 243;
+  const int ea2 = tid / 81, eS = tid - 81 * ea2;
+  double acc[27];
+#pragma unroll
+  for (int i = 0; i < 27; ++i) acc[i] = 0;
+  for (int p = 0; p < iters; ++p) {
+    if (MODE != 1 && w >= T8_F1W) t8_f1<double>(R + (p % T8_NRAW) * RS_SZ, P + ((p + 1) & 1) * PS_SZ, w - T8_F1W, lane);
+    if (MODE != 2 && unit) t8_f2<double>(P + (p & 1) * PS_SZ, ea2, eS, acc);
+    if (MODE != 3) __syncthreads();
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 27; ++i) s += acc[i];
+  if (s == 1234.5) *sink = s;
+}
+
+template <int MODE>
+float run(int grid, int iters, double* sink) {
+  auto k = k_pairs<MODE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T8Cfg<double>::SMEM);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k<<<grid, T8_NT, T8Cfg<double>::SMEM>>>(iters, sink);
+  cudaEventRecord(e0);
+  k<<<grid, T8_NT, T8Cfg<double>::SMEM>>>(iters, sink);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  return ms;
+}
+
+int main() {
+  int sms = 0, clk = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  double* sink;
+  cudaMalloc(&sink, 8);
+  const int iters = 20000;
+  const char* names[] = {"F1+F2+bar", "F2+bar", "F1+bar", "F1+F2 nobar"};
+  for (int ctas = 1; ctas <= 2; ++ctas) {
+    const int grid = sms * ctas;
+    for (int m = 0; m < 4; ++m) {
+      float ms = m == 0 ? run<0>(grid, iters, sink) : m == 1 ? run<1>(grid, iters, sink)
+               : m == 2 ? run<2>(grid, iters, sink) : run<3>(grid, iters, sink);
+      // clk per pair iteration per SM (all CTAs on the SM together)
+      const double clk_per = (ms * 1e-3) * (clk * 1e3) / ((double)iters * ctas);
+      printf("ctas/SM %d %-12s %.3f ms  %.0f clk per pair-iteration per SM\n", ctas, names[m], ms, clk_per);
+    }
+  }
+  printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+  return 0;
+}
