@@ -81,6 +81,7 @@ __device__ __forceinline__ void lds2(const uint64_t* p, uint64_t& a, uint64_t& b
 constexpr int T8_NW = 8;              // warps per tile CTA
 constexpr int T8_NT = 32 * T8_NW;     // 256 threads (243 tile units)
 constexpr int T8_F1W = 5;             // first of the three F1 warps
+constexpr int T8_SCHED = 128;         // scheduler / prefetch thread (warp 4 runs F2 only)
 // raw stage: op*RS_OP + b_a2*RS_H2 + b_a1*RS_H1 + b_B*8 + b_C, filled by 2 TMA copies of
 // 128 elements (the b_a2 halves of the natural slice) per operand; the pads put the F1
 // lanes (op, b_a2, b_C) on 32 distinct 8-byte bank slots (RS_H2 = 8, RS_OP = 16 mod 32)
@@ -134,11 +135,11 @@ __device__ __forceinline__ long long* ph_sh() {
   __shared__ long long s_ph[10];  // [0..7] phase sums, [8] thread-0 timestamp, [9] wait start
   return s_ph;
 }
-#define PH_DECL do { if (threadIdx.x == 0) { for (int i_ = 0; i_ < 8; ++i_) ph_sh()[i_] = 0; ph_sh()[8] = clock64(); } } while (0)
-#define PH_MARK(i) do { if (threadIdx.x == 0) { long long t_ = clock64(); ph_sh()[i] += t_ - ph_sh()[8]; ph_sh()[8] = t_; } } while (0)
+#define PH_DECL do { if (threadIdx.x == 128) { for (int i_ = 0; i_ < 8; ++i_) ph_sh()[i_] = 0; ph_sh()[8] = clock64(); } } while (0)
+#define PH_MARK(i) do { if (threadIdx.x == 128) { long long t_ = clock64(); ph_sh()[i] += t_ - ph_sh()[8]; ph_sh()[8] = t_; } } while (0)
 #define PH_WAIT_BEGIN(c) long long phw_ = (c) ? clock64() : 0
 #define PH_WAIT_END(c) do { if (c) atomicAdd((unsigned long long*)&ph_sh()[7], (unsigned long long)(clock64() - phw_)); } while (0)
-#define PH_FLUSH do { if (threadIdx.x == 0) for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&hc_phase[i_], (unsigned long long)ph_sh()[i_]); } while (0)
+#define PH_FLUSH do { if (threadIdx.x == 128) for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&hc_phase[i_], (unsigned long long)ph_sh()[i_]); } while (0)
 #else
 #define PH_DECL do { } while (0)
 #define PH_MARK(i) do { } while (0)
@@ -278,7 +279,7 @@ __device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, Raw
     else ++rr.done;
   };
 
-  if (tid == 0) pump();
+  if (tid == T8_SCHED) pump();
   f1(0, P);
   __syncthreads();
 
@@ -286,12 +287,12 @@ __device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, Raw
 #pragma unroll
   for (int i = 0; i < 27; ++i) acc[i] = T(0);
   for (int p = 0; p < npairs; ++p) {
-    if (tid == 0) pump();  // refill the stage F1(p) released
+    if (tid == T8_SCHED) pump();  // refill the stage F1(p) released
     if (p + 1 < npairs) f1(p + 1, P + ((p + 1) & 1) * PS_SZ);
     if (unit) t8_f2<T>(P + (p & 1) * PS_SZ, ea2, eS, acc);
     __syncthreads();
   }
-  if (tid == 0) {
+  if (tid == T8_SCHED) {
     pump();
     mid();  // no global stores of this CTA are in flight here: cheap place for a release
   }
@@ -333,7 +334,7 @@ __device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, Raw
 }
 
 __device__ __forceinline__ void ring_init(uint64_t* bars) {
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == T8_SCHED) {
     for (int i = 0; i < T8_NRAW; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -356,7 +357,7 @@ tile8_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z
   RawRing rr{raw_bar, 0, 0};
   const int k = D - 8;
   const uint64_t pol_in = policy_evict_last();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == T8_SCHED) {
     pf.left = 0;
     pf.pos = 0xffffffffu;  // next() moves to position 0
   }
@@ -504,7 +505,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
     }
   };
 
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == T8_SCHED) {
     uint32_t c[T8_QN];
     for (int i = 0; i < T8_QN; ++i) c[i] = atomicAdd(args.ctr, 1u);
     for (int i = 0; i < T8_QN; ++i) decode(c[i], s_slot[i]);
@@ -519,7 +520,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   ItemDec pd{};
   PH_DECL;
   while (true) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == T8_SCHED) {
       auto finish_pending = [&]() {  // complete the claim decoded one item ago
         Slot& o = s_slot[pslot];
         o.q = pq; o.p1 = pd.p1; o.j = pd.j; o.r = pd.r; o.loc = pov;
@@ -564,7 +565,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
     if (sel < 0) break;
     const Slot it = s_slot[sel];
     uint32_t claim = 0;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == T8_SCHED) {
       claim = atomicAdd(args.ctr, 1u);  // refills slot `sel` after this item
       cmask = 0;                         // snapshot the other pass-2 slots' slabs (used next time)
       for (int i = 0; i < T8_QN; ++i) {
@@ -579,7 +580,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
     T* zs = z + (uint64_t)it.loc * SLAB;
     if (it.p1) {
       if (skip1) {
-        if (threadIdx.x == 0) atomicAdd(done_ctr + it.j, 1u);
+        if (threadIdx.x == T8_SCHED) atomicAdd(done_ctr + it.j, 1u);
       } else {
         tile8<T, false>(1 << __popc(it.freeb), zs + (uint64_t)it.r * 6561ull, sm, rr, pol_keep, pump, signal);
         PH_MARK(6);
@@ -588,12 +589,12 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       // the slab's tiles are complete (a relaxed read of its counter saw N1, then the CTA
       // barrier): the reads below are ordered after it by that control dependency and the
       // barrier, and go to L2 (.cg), where the producers' fenced stores already are
-      if (threadIdx.x == 0) pump();
-      p2_item<T, M, 8>(zs, it.r, sm, threadIdx.x < 243 ? (int)threadIdx.x : -1, signal);
+      if (threadIdx.x == T8_SCHED) pump();
+      p2_item<T, M, 8>(zs, it.r, sm, threadIdx.x < 243 ? (int)threadIdx.x : -1, T8_SCHED, signal);
       PH_MARK(4);
     }
     __syncthreads();  // the item's smem is free
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == T8_SCHED) {
       if (it.p1 && !skip1) pend = it.j;  // published during the next item (or before a wait)
       if (pslot >= 0) {                  // finish the claim decoded one item ago
         Slot& o = s_slot[pslot];
