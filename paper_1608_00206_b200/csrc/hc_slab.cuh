@@ -7,7 +7,8 @@
 // axes; the paper's 4-way split (PAPER.md 166-177) on the k top axes (pair-sum).
 //
 // Tile axes (bit / trit b of the tile index, b = 0 fastest):
-//   C = {0,1,2}  register axes: 27 accumulators per thread
+//   C = {0,1,2}  register axes: 27 accumulators per thread (Karatsuba on axis 2, the direct
+//                split on axes 0, 1: see kdd_mul_acc)
 //   B = {3,4,5}  evaluated by the F1 warps, in registers
 //   a1 = 6       evaluated by the F1 warps (one warp per evaluation point e_a1)
 //   a2 = 7       summed by the F2 threads while they load (e_a2 = 1: two rows)
@@ -80,8 +81,13 @@ __device__ __forceinline__ void lds2(const uint64_t* p, uint64_t& a, uint64_t& b
 // ---- layouts (element offsets) ------------------------------------------------------
 constexpr int T8_NW = 8;              // warps per tile CTA
 constexpr int T8_NT = 32 * T8_NW;     // 256 threads (243 tile units)
-constexpr int T8_F1W = 5;             // first of the three F1 warps
-constexpr int T8_SCHED = 128;         // scheduler / prefetch thread (warp 4 runs F2 only)
+// Warp roles, balanced so that every warp does about the same work between barriers:
+//   threads 0..80 own the e_a2 = 1 units (two rows per F2 load: warps 0, 1, part of 2),
+//   threads 81..161 the e_a2 = 0 units, 162..242 the e_a2 = 2 units;
+//   F1 runs on warps 3, 4, 6 (single-row F2), e_s = 0, 1, 2; the scheduler on warp 7.
+__device__ __forceinline__ int t8_unit(int tid) { return tid < 81 ? tid + 81 : (tid < 162 ? tid - 81 : tid); }
+__device__ __forceinline__ int t8_f1_es(int w) { return w == 3 ? 0 : (w == 4 ? 1 : (w == 6 ? 2 : -1)); }
+constexpr int T8_SCHED = 224;         // scheduler / prefetch thread (warp 7: light F2, no F1)
 // raw stage: op*RS_OP + b_a2*RS_H2 + b_a1*RS_H1 + b_B*8 + b_C, filled by 2 TMA copies of
 // 128 elements (the b_a2 halves of the natural slice) per operand; the pads put the F1
 // lanes (op, b_a2, b_C) on 32 distinct 8-byte bank slots (RS_H2 = 8, RS_OP = 16 mod 32)
@@ -177,7 +183,7 @@ __device__ __forceinline__ uint32_t t8_wait(RawRing& rr) {
   return st;
 }
 
-// Stage F1 of one pair (warps T8_F1W + e_s): lane (op, b_a2, b_C) evaluates the a1 axis at
+// Stage F1 of one pair (warp with t8_f1_es(w) = e_s): lane (op, b_a2, b_C) evaluates the a1 axis at
 // e_s and the three B axes (PAPER.md 186-189 per axis), and stores the 27 values e_B.
 template <class T>
 __device__ __forceinline__ void t8_f1(const T* R, T* P, int es, int lane) {
@@ -228,7 +234,10 @@ __device__ __forceinline__ void t8_f2(const T* P, int ea2, int eS, T* acc) {
       yt[j + 1] = Ar<T>::add(yt[j + 1], v1);
     }
   }
-  fwd_mul_acc<3, T>(xt, yt, acc);
+  // fp64: FMA-bound, the Karatsuba/direct mix is cheaper; uint64: a 64-bit multiply costs
+  // several integer instructions, so Karatsuba on all three axes stays cheaper
+  if constexpr (sizeof(T) == 8 && T(0.5) != T(0)) kdd_mul_acc<T>(xt, yt, acc);
+  else fwd_mul_acc<3, T>(xt, yt, acc);
 }
 
 // Prefetch cursor (shared memory, thread 0 only) over the pairs of the pass-1 items in the
@@ -271,11 +280,13 @@ __device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, Raw
   T* R = sm + T8Cfg<T>::ALIAS;        // [T8_NRAW][RS_SZ]
   T* S = sm;                          // [9][27][27] after the pair loop (aliases P)
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const bool unit = tid < 243;                     // F2 / inverse unit (e_a2, e_S)
-  const int ea2 = tid / 81, eS = tid - 81 * ea2;   // e_S = e_B + 27 e_a1
-  // F1: warps T8_F1W + e_s evaluate a1 at e_s (the other warps only advance the ring count)
+  const bool unit = tid < 243;                     // F2 / inverse unit u = (e_a2, e_S)
+  const int u = t8_unit(tid);
+  const int ea2 = u / 81, eS = u - 81 * ea2;       // e_S = e_B + 27 e_a1
+  const int f1es = t8_f1_es(w);
+  // F1: the warp with f1es = e_s evaluates a1 at e_s (the others only advance the ring count)
   auto f1 = [&](int, T* Pd) {
-    if (w >= T8_F1W) t8_f1<T>(R + t8_wait(rr) * RS_SZ, Pd, w - T8_F1W, lane);
+    if (f1es >= 0) t8_f1<T>(R + t8_wait(rr) * RS_SZ, Pd, f1es, lane);
     else ++rr.done;
   };
 
@@ -299,11 +310,13 @@ __device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, Raw
   PH_MARK(1);
 
   // a4: inverse on the C register axes, then B (SMEM exchange), then A + store (a6).
-  // Unit u = (e_A, e_B) with e_A = e_a1 + 3 e_a2, so S[e_A][e_B][k_C] = S[27 u + k_C].
+  // Unit u = (e_A, e_B) with e_A = e_a1 + 3 e_a2, so S[e_A][e_B][k_C] = S[27 u + k_C]
+  // (stride 27: conflict-free whatever the thread-to-unit map).
   if (unit) {
-    inv_reg<3, T>(acc);
+    if constexpr (T(0.5) != T(0)) inv_top3<T>(acc);  // fp64: the lower register axes were direct
+    else inv_reg<3, T>(acc);
 #pragma unroll
-    for (int i = 0; i < 27; ++i) S[tid * 27 + i] = acc[i];
+    for (int i = 0; i < 27; ++i) S[u * 27 + i] = acc[i];
   }
   __syncthreads();
   if (unit) {  // unit (e_A, k_C): interpolate the B axes

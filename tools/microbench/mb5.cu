@@ -17,12 +17,13 @@ __global__ void __launch_bounds__(T8_NT, 2) k_pairs(int iters, double* sink) {
   __syncthreads();
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const bool unit = tid < 243;
-  const int ea2 = tid / 81, eS = tid - 81 * ea2;
+  const int uu = t8_unit(tid);
+  const int ea2 = uu / 81, eS = uu - 81 * ea2;
   double acc[27];
 #pragma unroll
   for (int i = 0; i < 27; ++i) acc[i] = 0;
   for (int p = 0; p < iters; ++p) {
-    if (MODE != 1 && w >= T8_F1W) t8_f1<double>(R + (p % T8_NRAW) * RS_SZ, P + ((p + 1) & 1) * PS_SZ, w - T8_F1W, lane);
+    if (MODE != 1 && t8_f1_es(w) >= 0) t8_f1<double>(R + (p % T8_NRAW) * RS_SZ, P + ((p + 1) & 1) * PS_SZ, t8_f1_es(w), lane);
     if (MODE != 2 && unit) t8_f2<double>(P + (p & 1) * PS_SZ, ea2, eS, acc);
     if (MODE != 3) __syncthreads();
   }
