@@ -20,7 +20,8 @@
  * Ownership: the caller owns x, y, z.  x and y are never modified (unlike Algorithm 2,
  *   PAPER.md 225, which destroys its inputs).  z must not alias x or y.  A plan owns
  *   only small tables, its own device buffers for the host-pointer entry point, and
- *   counters.  Pointers must be 16-byte aligned (torch allocations are 256-B aligned).
+ *   counters.  x and y must be 16-byte aligned (their slices are staged by TMA bulk copies),
+ *   z 8-byte aligned (one element); torch allocations are 256-B aligned.
  * Streams: all device work is enqueued on `stream` (a cudaStream_t passed as void*;
  *   NULL = legacy default stream).  Calls return after enqueueing; launch errors are
  *   reported immediately (HC_ERR_CUDA); execution errors surface at the caller's sync.
@@ -47,7 +48,7 @@ typedef enum {
     HC_ERR_INVALID_DIM = 1,  /* D outside [1, HC_MAX_D], or B < 1 */
     HC_ERR_DTYPE = 2,        /* unknown hc_dtype */
     HC_ERR_NULL = 3,         /* a required pointer is NULL */
-    HC_ERR_ALIGN = 4,        /* a pointer is not 16-byte aligned */
+    HC_ERR_ALIGN = 4,        /* x or y not 16-byte aligned, or z not 8-byte aligned */
     HC_ERR_DEVICE = 5,       /* no CUDA device / wrong architecture (needs sm_100) */
     HC_ERR_CAPACITY = 6,     /* device memory cannot hold the requested buffers */
     HC_ERR_CUDA = 7,         /* a CUDA runtime call or kernel launch failed */
@@ -101,6 +102,35 @@ hc_status hc_convolve_batched(int B, int D, hc_dtype dtype, const void* x, const
  * Synchronous: returns after z_host is complete. */
 hc_status hc_convolve_host(hc_plan_t plan, const void* x_host, const void* y_host,
                            void* z_host, void* stream);
+
+/* ---- Evaluation-point variant of the multi-GPU split (BASELINE.json north_star (4);
+ * SURVEY.md §8(e) "K5b").  The top k axes (1 <= k <= 4, k < D) use the paper's Karatsuba
+ * split (PAPER.md 185-192) ACROSS ranks: rank r owns the evaluation points
+ * e_T in [e_begin, e_end) of {0,1,2}^k (flat base-3 index, trit b = axis D-k+b) and computes
+ *     w[e_T][.] = conv_{D-k}( xh[e_T], yh[e_T] ),   xh[e_T][i_L] = sum_{i_T ~ e_T} x[i_T][i_L]
+ * (the forward over the top axes -- a0, a0 + a1, a1 per axis -- then the whole
+ * (D-k)-dimensional convolution with this library's engine).  An all-to-all, done by the
+ * caller (NCCL send/recv or peer copies), gives rank h the columns [col_begin, col_end) of
+ * w for all 3^k points; hc_ep_finish then interpolates over the top k axes,
+ *     z[k_T][col] = sum_{e_T} Inv[k_T][e_T] w[e_T][col],  per axis (c0, (c1-c0)-c2, c2),
+ * PAPER.md 187-189 / 248-251.  Rank h's output is the 3^k strided chunks
+ * z[k_T * 3^(D-k) + col], col in its column range, delivered dense as [3^k][ncols]. */
+typedef struct hc_ep_s* hc_ep_t;
+
+/* Pure host: the evaluation points [e_begin, e_end) and columns [col_begin, col_end) of
+ * `rank` (contiguous, disjoint, in rank order, sizes differing by at most one).
+ * Requires ngpu <= 3^k; HC_ERR_SHARD otherwise. */
+hc_status hc_ep_range(int D, int k, int ngpu, int rank, uint64_t* e_begin, uint64_t* e_end,
+                      uint64_t* col_begin, uint64_t* col_end);
+/* Plan for one rank (owns the (D-k)-dimensional plan and 2 x 2^(D-k) elements of scratch). */
+hc_status hc_ep_create(hc_ep_t* out, int D, int k, hc_dtype dtype, int ngpu, int rank);
+hc_status hc_ep_destroy(hc_ep_t p);
+/* Local step: x, y (2^D each, device, replicated); w (device) receives
+ * (e_end - e_begin) x 3^(D-k) elements, row e_T - e_begin. */
+hc_status hc_ep_local(hc_ep_t p, const void* x, const void* y, void* w, void* stream);
+/* Final step: wt = [3^k][ncols] gathered columns of w (device), z = [3^k][ncols] (device),
+ * ncols = col_end - col_begin; z must not alias wt. */
+hc_status hc_ep_finish(hc_ep_t p, const void* wt, void* z, void* stream);
 
 /* Instrumentation (for bench.py / tests): cumulative number of kernels this library has
  * launched in this process, and per-kernel device time when profiling is enabled

@@ -89,7 +89,7 @@ extern "C" const char* hc_status_str(hc_status s) {
     case HC_ERR_INVALID_DIM: return "invalid dimension (need 1 <= D <= HC_MAX_D, B >= 1)";
     case HC_ERR_DTYPE: return "unknown dtype";
     case HC_ERR_NULL: return "null pointer";
-    case HC_ERR_ALIGN: return "pointer not 16-byte aligned";
+    case HC_ERR_ALIGN: return "x / y not 16-byte aligned, or z not 8-byte aligned";
     case HC_ERR_DEVICE: return "no usable CUDA device (needs sm_100)";
     case HC_ERR_CAPACITY: return "insufficient device memory";
     case HC_ERR_CUDA: return "CUDA error";
@@ -106,6 +106,7 @@ namespace {
 constexpr int kTileL = 8;  // low axes handled inside one CTA (3^8 = 6561 outputs)
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
 
 // Device capability check, cached per device (cudaGetDeviceProperties is slow).
 hc_status check_device() {
@@ -465,13 +466,13 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
 
 extern "C" hc_status hc_convolve(hc_plan_t p, const void* x, const void* y, void* z, void* stream) {
   if (!p || !x || !y || !z) return HC_ERR_NULL;
-  if (!aligned16(x) || !aligned16(y) || !aligned16(z)) return HC_ERR_ALIGN;
+  if (!aligned16(x) || !aligned16(y) || !aligned8(z)) return HC_ERR_ALIGN;
   return run_range(p, x, y, z, 0, p->g.nunits, (cudaStream_t)stream, 0);
 }
 
 extern "C" hc_status hc_convolve_sharded(hc_plan_t p, const void* x, const void* y, void* zs, void* stream) {
   if (!p || !x || !y || !zs) return HC_ERR_NULL;
-  if (!aligned16(x) || !aligned16(y) || !aligned16(zs)) return HC_ERR_ALIGN;
+  if (!aligned16(x) || !aligned16(y) || !aligned8(zs)) return HC_ERR_ALIGN;
   return run_range(p, x, y, zs, p->cuts[p->rank], p->cuts[p->rank + 1], (cudaStream_t)stream, 0);
 }
 
@@ -480,7 +481,7 @@ extern "C" hc_status hc_convolve_batched(int B, int D, hc_dtype dtype, const voi
   if (B < 1 || D < 1 || D > HC_MAX_D) return HC_ERR_INVALID_DIM;
   if (dtype != HC_INT64 && dtype != HC_FP64) return HC_ERR_DTYPE;
   if (!x || !y || !z) return HC_ERR_NULL;
-  if (!aligned16(x) || !aligned16(y) || !aligned16(z)) return HC_ERR_ALIGN;
+  if (!aligned16(x) || !aligned16(y) || !aligned8(z)) return HC_ERR_ALIGN;
   hc_status ds = check_device();
   if (ds != HC_OK) return ds;
   const int L = D < kTileL ? D : kTileL;
@@ -537,4 +538,118 @@ extern "C" hc_status hc_convolve_host(hc_plan_t p, const void* xh, const void* y
   cudaError_t e2 = cudaStreamSynchronize(p->hs[1]);
   cudaEventDestroy(ready);
   return (e1 == cudaSuccess && e2 == cudaSuccess) ? HC_OK : HC_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------------------------------
+// Evaluation-point variant (include/hc.h, hc_ep_*; kernels in hc_ep.cuh).
+#include "hc_ep.cuh"
+
+struct hc_ep_s {
+  int D, k, ngpu, rank;
+  hc_dtype dtype;
+  uint64_t e0, e1, c0, c1;   // owned evaluation points and columns
+  hc_plan_t low = nullptr;   // plan of the (D-k)-dimensional convolution
+  void* xh = nullptr;        // forward-evaluated operands of one point (2^(D-k) each)
+  void* yh = nullptr;
+};
+
+extern "C" hc_status hc_ep_range(int D, int k, int ngpu, int rank, uint64_t* e_begin, uint64_t* e_end,
+                                 uint64_t* col_begin, uint64_t* col_end) {
+  if (!e_begin || !e_end || !col_begin || !col_end) return HC_ERR_NULL;
+  if (D < 2 || D > HC_MAX_D || k < 1 || k > 4 || k >= D) return HC_ERR_INVALID_DIM;
+  const uint64_t np = upow3(k), nc = upow3(D - k);
+  if (ngpu < 1 || rank < 0 || rank >= ngpu || (uint64_t)ngpu > np) return HC_ERR_SHARD;
+  *e_begin = np * (uint64_t)rank / (uint64_t)ngpu;
+  *e_end = np * (uint64_t)(rank + 1) / (uint64_t)ngpu;
+  *col_begin = nc * (uint64_t)rank / (uint64_t)ngpu;
+  *col_end = nc * (uint64_t)(rank + 1) / (uint64_t)ngpu;
+  return HC_OK;
+}
+
+extern "C" hc_status hc_ep_create(hc_ep_t* out, int D, int k, hc_dtype dtype, int ngpu, int rank) {
+  if (!out) return HC_ERR_NULL;
+  *out = nullptr;
+  if (dtype != HC_INT64 && dtype != HC_FP64) return HC_ERR_DTYPE;
+  auto* p = new hc_ep_s();
+  p->D = D; p->k = k; p->ngpu = ngpu; p->rank = rank; p->dtype = dtype;
+  hc_status s = hc_ep_range(D, k, ngpu, rank, &p->e0, &p->e1, &p->c0, &p->c1);
+  if (s == HC_OK) s = hc_plan_create(&p->low, D - k, dtype, 1, 0);
+  if (s == HC_OK) {
+    const size_t bytes = sizeof(double) * (1ull << (D - k));
+    if (cudaMalloc(&p->xh, bytes) != cudaSuccess || cudaMalloc(&p->yh, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      s = HC_ERR_CAPACITY;
+    }
+  }
+  if (s != HC_OK) {
+    hc_ep_destroy(p);
+    return s;
+  }
+  *out = p;
+  return HC_OK;
+}
+
+extern "C" hc_status hc_ep_destroy(hc_ep_t p) {
+  if (!p) return HC_ERR_NULL;
+  if (p->low) hc_plan_destroy(p->low);
+  cudaFree(p->xh);
+  cudaFree(p->yh);
+  delete p;
+  return HC_OK;
+}
+
+namespace {
+template <class T>
+cudaError_t ep_local_t(hc_ep_t p, const T* x, const T* y, T* w, cudaStream_t st) {
+  const int L = p->D - p->k;
+  const uint64_t nout = upow3(L);
+  for (uint64_t e = p->e0; e < p->e1; ++e) {
+    uint32_t base = 0, freeb = 0;
+    uint64_t t = e;
+    for (int a = 0; a < p->k; ++a, t /= 3) {
+      if (t % 3 == 2) base |= 1u << a;
+      else if (t % 3 == 1) freeb |= 1u << a;
+    }
+    {
+      LaunchScope ls("ep_eval", st);
+      dim3 g((unsigned)(((1ull << L) + 255) / 256), 2);
+      ep_eval_kernel<T><<<g, 256, 0, st>>>(x, y, (T*)p->xh, (T*)p->yh, L, base, freeb);
+      cudaError_t err = cudaGetLastError();
+      if (err != cudaSuccess) return err;
+    }
+    if (hc_convolve(p->low, p->xh, p->yh, w + (e - p->e0) * nout, st) != HC_OK) return cudaErrorLaunchFailure;
+  }
+  return cudaSuccess;
+}
+template <class T>
+cudaError_t ep_finish_t(hc_ep_t p, const T* wt, T* z, cudaStream_t st) {
+  const uint64_t ncols = p->c1 - p->c0;
+  if (ncols == 0) return cudaSuccess;
+  const unsigned g = (unsigned)((ncols + 127) / 128);
+  LaunchScope ls("ep_inverse", st);
+  switch (p->k) {
+    case 1: ep_top_inverse<T, 1><<<g, 128, 0, st>>>(wt, z, ncols); break;
+    case 2: ep_top_inverse<T, 2><<<g, 128, 0, st>>>(wt, z, ncols); break;
+    case 3: ep_top_inverse<T, 3><<<g, 128, 0, st>>>(wt, z, ncols); break;
+    default: ep_top_inverse<T, 4><<<g, 128, 0, st>>>(wt, z, ncols); break;
+  }
+  return cudaGetLastError();
+}
+}  // namespace
+
+extern "C" hc_status hc_ep_local(hc_ep_t p, const void* x, const void* y, void* w, void* stream) {
+  if (!p || !x || !y || !w) return HC_ERR_NULL;
+  if (!aligned16(x) || !aligned16(y) || !aligned8(w)) return HC_ERR_ALIGN;
+  cudaError_t e = p->dtype == HC_INT64
+                      ? ep_local_t<uint64_t>(p, (const uint64_t*)x, (const uint64_t*)y, (uint64_t*)w, (cudaStream_t)stream)
+                      : ep_local_t<double>(p, (const double*)x, (const double*)y, (double*)w, (cudaStream_t)stream);
+  return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
+}
+
+extern "C" hc_status hc_ep_finish(hc_ep_t p, const void* wt, void* z, void* stream) {
+  if (!p || !wt || !z) return HC_ERR_NULL;
+  cudaError_t e = p->dtype == HC_INT64
+                      ? ep_finish_t<uint64_t>(p, (const uint64_t*)wt, (uint64_t*)z, (cudaStream_t)stream)
+                      : ep_finish_t<double>(p, (const double*)wt, (double*)z, (cudaStream_t)stream);
+  return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
 }

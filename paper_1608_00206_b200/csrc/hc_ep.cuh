@@ -1,0 +1,47 @@
+// hc_ep.cuh -- kernels of the evaluation-point variant of the multi-GPU split
+// (BASELINE.json north_star (4); SURVEY.md §8(e) "K5b"; C ABI in include/hc.h, hc_ep_*).
+//
+// The top k axes use the paper's Karatsuba split (PAPER.md 185-192) across ranks:
+//   ep_eval_kernel   xh[e_T][i_L] = sum_{i_T ~ e_T} x[i_T][i_L]  (forward over the top axes,
+//                    (a0, a0 + a1, a1) per axis; subsets in ascending order)
+//   (the (D-k)-dimensional convolution of xh, yh runs on the slab / tile engines)
+//   ep_top_inverse   z[k_T][col] = inverse over the top axes of w[.][col]
+//                    ((c0, (c1 - c0) - c2, c2) per axis, PAPER.md 187-189, 248-251)
+#pragma once
+#include "hc_tile.cuh"
+
+namespace hc {
+
+// grid (ceil(2^L / 256), 2 operands), block 256: one evaluation point e_T of the top k axes
+template <class T>
+__global__ void __launch_bounds__(256) ep_eval_kernel(const T* __restrict__ x, const T* __restrict__ y,
+                                                      T* __restrict__ xh, T* __restrict__ yh, int L,
+                                                      uint32_t base, uint32_t freeb) {
+  const uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i >= (1ull << L)) return;
+  const T* src = (blockIdx.y ? y : x) + i;
+  T acc = T(0);
+  uint32_t s = 0;
+  do {
+    acc = Ar<T>::add(acc, __ldg(src + ((uint64_t)(base | s) << L)));
+    s = (s - freeb) & freeb;
+  } while (s != 0);
+  (blockIdx.y ? yh : xh)[i] = acc;
+}
+
+// one thread per column: load the 3^K evaluation values (coalesced across threads),
+// interpolate over the K top axes in registers, store the 3^K outputs
+template <class T, int K>
+__global__ void __launch_bounds__(128) ep_top_inverse(const T* __restrict__ wt, T* __restrict__ z, uint64_t ncols) {
+  const uint64_t col = (uint64_t)blockIdx.x * 128 + threadIdx.x;
+  if (col >= ncols) return;
+  constexpr int NP = ipow3(K);
+  T v[NP];
+#pragma unroll
+  for (int e = 0; e < NP; ++e) v[e] = wt[(uint64_t)e * ncols + col];
+  inv_reg<K, T>(v);
+#pragma unroll
+  for (int e = 0; e < NP; ++e) st_cs(z + (uint64_t)e * ncols + col, v[e]);
+}
+
+}  // namespace hc

@@ -39,6 +39,11 @@ _lib.hc_convolve.argtypes = [_P, _P, _P, _P, _P]
 _lib.hc_convolve_sharded.argtypes = [_P, _P, _P, _P, _P]
 _lib.hc_convolve_batched.argtypes = [_I, _I, _I, _P, _P, _P, _P]
 _lib.hc_convolve_host.argtypes = [_P, _P, _P, _P, _P]
+_lib.hc_ep_range.argtypes = [_I, _I, _I, _I] + [ctypes.POINTER(_U64)] * 4
+_lib.hc_ep_create.argtypes = [ctypes.POINTER(_P), _I, _I, _I, _I, _I]
+_lib.hc_ep_destroy.argtypes = [_P]
+_lib.hc_ep_local.argtypes = [_P, _P, _P, _P, _P]
+_lib.hc_ep_finish.argtypes = [_P, _P, _P, _P]
 _lib.hc_launch_count.restype = _U64
 _lib.hc_prof_enable.argtypes = [_I]
 _lib.hc_prof_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_U64)]
@@ -182,6 +187,82 @@ def convolve(x, y, z=None, stream=None):
         z = torch.empty(3 ** D, dtype=x.dtype, device=x.device)
     Plan(D, x.dtype).convolve(x, y, z, stream)
     return z
+
+
+def ep_range(D: int, k: int, ngpu: int, rank: int):
+    """Host-only (hc_ep_range): ((e_begin, e_end), (col_begin, col_end)) of `rank`."""
+    v = [_U64() for _ in range(4)]
+    _ok(_lib.hc_ep_range(D, k, ngpu, rank, *[ctypes.byref(t) for t in v]), "hc_ep_range")
+    return (int(v[0].value), int(v[1].value)), (int(v[2].value), int(v[3].value))
+
+
+class EPPlan:
+    """Evaluation-point variant of the multi-GPU split (hc_ep_*; BASELINE north_star (4)).
+
+    local(x, y, w): w[(e - e_begin), :] = conv_{D-k}(forward_top(x)[e], forward_top(y)[e]);
+    exchange (ep_exchange, NCCL send/recv); finish(wt, z): interpolation over the top axes."""
+
+    def __init__(self, D: int, k: int, dtype="float64", ngpu: int = 1, rank: int = 0):
+        self.D, self.k, self.ngpu, self.rank = D, k, ngpu, rank
+        self.dtype_code = _dtype_code(dtype)
+        (self.e0, self.e1), (self.c0, self.c1) = ep_range(D, k, ngpu, rank)
+        self.npoints, self.ncols_total = 3 ** k, 3 ** (D - k)
+        h = _P()
+        _ok(_lib.hc_ep_create(ctypes.byref(h), D, k, self.dtype_code, ngpu, rank), "hc_ep_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.hc_ep_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def local(self, x, y, w, stream=None):
+        n = in_len(self.D)
+        _ok(_lib.hc_ep_local(self._h, _dev(x, n, self.dtype_code, "x"), _dev(y, n, self.dtype_code, "y"),
+                             _dev(w, (self.e1 - self.e0) * self.ncols_total, self.dtype_code, "w"),
+                             _P(_stream_ptr(stream))), "hc_ep_local")
+        return w
+
+    def finish(self, wt, z, stream=None):
+        m = self.npoints * (self.c1 - self.c0)
+        _ok(_lib.hc_ep_finish(self._h, _dev(wt, m, self.dtype_code, "wt"), _dev(z, m, self.dtype_code, "z"),
+                              _P(_stream_ptr(stream))), "hc_ep_finish")
+        return z
+
+
+def ep_exchange(w, wt, D: int, k: int, rank: int, world: int, dist=None):
+    """The all-to-all of the evaluation-point variant: rank g holds w[e - e_begin_g, :] for
+    its points; afterwards wt[e, :] = w_of_owner(e)[e, col_begin_rank : col_end_rank] for all
+    3^k points.  Point-to-point NCCL (or gloo) sends of contiguous row segments in one
+    batch.  world == 1: a device copy."""
+    ranges = [ep_range(D, k, world, r) for r in range(world)]
+    (e0, e1), (c0, c1) = ranges[rank]
+    if world == 1 or dist is None:
+        wt.view(e1 - e0, c1 - c0).copy_(w.view(e1 - e0, -1)[:, c0:c1])
+        return wt
+    wv = w.view(e1 - e0, -1)
+    wtv = wt.view(3 ** k, c1 - c0)
+    ops = []
+    for h in range(world):
+        (_, _), (hc0, hc1) = ranges[h]
+        (he0, he1), _ = ranges[h]
+        if h == rank:
+            wtv[e0:e1].copy_(wv[:, c0:c1])
+            continue
+        for e in range(e0, e1):
+            ops.append(dist.P2POp(dist.isend, wv[e - e0, hc0:hc1].contiguous(), h))
+        for e in range(he0, he1):
+            ops.append(dist.P2POp(dist.irecv, wtv[e], h))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return wt
 
 
 def launch_count() -> int:

@@ -197,3 +197,109 @@ def test_errors(hc):
     with pytest.raises(hc.HCError) as ei:
         p.convolve(buf[1:17], buf[1:17], torch.empty(81, dtype=torch.int64, device="cuda"))
     assert ei.value.code == 4
+
+
+@pytest.mark.parametrize("D,dtype", [(13, "float64"), (14, "int64"), (15, "float64")])
+def test_two_level_geometries(hc, orc, D, dtype):
+    # D = 13: slab of 13 axes (M = 5), no top axes; 14: M = 6, k = 0; 15: M = 6, k = 1
+    # (DESIGN.md §4): every cell against Algorithm 1
+    if dtype == "int64":
+        x, y = hcgen.make_pair(D, "int64", "uniform", 500 + D, -(1 << 20), 1 << 20)
+    else:
+        x, y = hcgen.make_pair(D, "float64", "exp_norm", 500 + D)
+    got = _run(hc, x, y).cpu().numpy()
+    _assert_close(got, orc.conv(x, y), x, y)
+
+
+def test_d17_int64_sampled_and_ragged_shards(hc, orc):
+    # k = 3 top axes, uneven shards (3 ranks over 27 slabs): concatenation = full output,
+    # sampled cells (whole first/last slab tiles included) against the oracle
+    D = 17
+    x, y = hcgen.make_pair(D, "int64", "uniform", 1717, 0, 1 << 16)
+    full = _run(hc, x, y)
+    xs, ys = _gpu(x), _gpu(y)
+    parts = []
+    for r in range(3):
+        p = hc.Plan(D, "int64", 3, r)
+        b, e = p.shard_info()
+        zs = torch.empty(e - b, dtype=torch.int64, device="cuda")
+        p.convolve_sharded(xs, ys, zs)
+        parts.append(zs)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts), full)
+    ks = _sample_cells(D, 20000, 17)
+    got = full[torch.from_numpy(ks).cuda()].cpu().numpy()
+    assert np.array_equal(got, orc.conv_cells(x, y, ks.astype(np.uint64)))
+
+
+@pytest.mark.slow
+def test_config_c5_d22_one_shard_of_eight(hc, orc):
+    # BASELINE config 5 (D = 22 fp64, 251 GB of output) does not fit one GPU: compute the
+    # shard of rank 5 of 8 (the launch configuration of the 8-GPU run) and check sampled
+    # cells of it against the oracle, plus the shard's share of the mass.
+    D, n, r = 22, 8, 5
+    x, y = hcgen.config_inputs("c5_d22_f64")
+    p = hc.Plan(D, "float64", n, r)
+    b, e = p.shard_info()
+    zs = torch.empty(e - b, dtype=torch.float64, device="cuda")
+    p.convolve_sharded(_gpu(x), _gpu(y), zs)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(22)
+    loc = np.unique(np.concatenate([rng.integers(0, e - b, 4000), np.arange(0, 3 ** 8),
+                                    np.arange(e - b - 3 ** 8, e - b)]))
+    got = zs[torch.from_numpy(loc).cuda()].cpu().numpy()
+    want = orc.conv_cells(x, y, (loc + b).astype(np.uint64))
+    _assert_close(got, want, x, y)
+    assert torch.isfinite(zs).all()
+    del zs
+
+
+@pytest.mark.parametrize("D,k,dtype,nranks", [(11, 1, "int64", 2), (11, 2, "int64", 5), (12, 3, "int64", 3),
+                                              (12, 4, "int64", 8), (10, 2, "float64", 4), (14, 4, "int64", 1)])
+def test_evalpoint_variant_emulated_ranks(hc, orc, D, k, dtype, nranks):
+    # north_star (4): every rank's local step, the exchange emulated on one device (each rank's
+    # columns gathered from all ranks' w), the top-axes interpolation; the 3^k strided chunks
+    # of each rank must equal Algorithm 1 (int64 bit-exact)
+    if dtype == "int64":
+        x, y = hcgen.make_pair(D, "int64", "uniform", 900 + D + k, -300, 300)
+    else:
+        x, y = hcgen.make_pair(D, "float64", "exp_norm", 900 + D + k)
+    want = orc.conv(x, y)
+    tdt = torch.int64 if dtype == "int64" else torch.float64
+    xs, ys = _gpu(x), _gpu(y)
+    nc, npnt = 3 ** (D - k), 3 ** k
+    plans = [hc.EPPlan(D, k, dtype, nranks, r) for r in range(nranks)]
+    W = torch.empty((npnt, nc), dtype=tdt, device="cuda")
+    for p in plans:
+        w = torch.empty((p.e1 - p.e0) * nc, dtype=tdt, device="cuda")
+        p.local(xs, ys, w)
+        W[p.e0:p.e1] = w.view(-1, nc)
+    got = np.empty(3 ** D, dtype=want.dtype)
+    for p in plans:
+        wt = W[:, p.c0:p.c1].contiguous().view(-1)
+        z = torch.empty_like(wt)
+        p.finish(wt, z)
+        torch.cuda.synchronize()
+        got.reshape(npnt, nc)[:, p.c0:p.c1] = z.view(npnt, -1).cpu().numpy()
+    _assert_close(got, want, x, y)
+    if nranks == 1:  # world 1: ep_exchange is the identity copy
+        p = plans[0]
+        w = torch.empty(npnt * nc, dtype=tdt, device="cuda")
+        p.local(xs, ys, w)
+        wt = torch.empty_like(w)
+        hc.ep_exchange(w, wt, D, k, 0, 1)
+        z = torch.empty_like(w)
+        p.finish(wt, z)
+        torch.cuda.synchronize()
+        _assert_close(z.cpu().numpy(), want, x, y)
+
+
+def test_output_at_odd_element_offset(hc, orc):
+    # z only needs element (8-byte) alignment: write into a view that starts one element in
+    for D in (7, 9, 13):
+        x, y = hcgen.make_pair(D, "int64", "uniform", 4242 + D, -50, 50)
+        buf = torch.zeros(3 ** D + 1, dtype=torch.int64, device="cuda")
+        hc.Plan(D, "int64").convolve(_gpu(x), _gpu(y), buf[1:])
+        torch.cuda.synchronize()
+        assert int(buf[0]) == 0
+        assert np.array_equal(buf[1:].cpu().numpy(), orc.conv(x, y))

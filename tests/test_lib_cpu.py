@@ -101,3 +101,23 @@ def test_shard_errors(hc):
         hc.shard_range(20, 2, 2)
     with pytest.raises(hc.HCError):
         hc.shard_range(8, 2, 0)   # a single slab cannot be split
+
+
+@pytest.mark.parametrize("D,k", [(6, 1), (12, 3), (20, 4), (22, 4)])
+def test_ep_ranges_partition(hc, D, k):
+    # evaluation-point variant (hc_ep_range): points and columns are split contiguously,
+    # disjointly, in rank order, sizes within one of each other
+    for n in [1, 2, 3, 8, 3 ** k]:
+        if n > 3 ** k:
+            continue
+        rs = [hc.ep_range(D, k, n, r) for r in range(n)]
+        for which, total in ((0, 3 ** k), (1, 3 ** (D - k))):
+            segs = [r[which] for r in rs]
+            assert segs[0][0] == 0 and segs[-1][1] == total
+            assert all(segs[i][1] == segs[i + 1][0] for i in range(n - 1))
+            sizes = [b - a for a, b in segs]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(hc.HCError):
+        hc.ep_range(D, k, 3 ** k + 1, 0)
+    with pytest.raises(hc.HCError):
+        hc.ep_range(D, 5, 1, 0)

@@ -59,3 +59,45 @@ def test_two_rank_partition_and_timing(D):
     assert ranges[0][1] == ranges[1][0]
     for _, _, t in res:
         assert t == [10.0 + world - 1, 3.0 * world]   # max over ranks, elementwise
+
+
+def _ep_worker(rank, world, port, D, k, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1608_00206_b200.hc as hc
+        (e0, e1), (c0, c1) = hc.ep_range(D, k, world, rank)
+        nc = 3 ** (D - k)
+        # w rows of this rank's points, value = e * 10^6 + column (exact in float64)
+        e = torch.arange(e0, e1, dtype=torch.float64).view(-1, 1)
+        w = (e * 1e6 + torch.arange(nc, dtype=torch.float64).view(1, -1)).reshape(-1)
+        wt = torch.full(((3 ** k) * (c1 - c0),), -1.0, dtype=torch.float64)
+        hc.ep_exchange(w, wt, D, k, rank, world, dist)
+        want = (torch.arange(3 ** k, dtype=torch.float64).view(-1, 1) * 1e6
+                + torch.arange(c0, c1, dtype=torch.float64).view(1, -1)).reshape(-1)
+        q.put((rank, bool(torch.equal(wt, want))))
+    except Exception as ex:  # report instead of leaving the parent waiting on the queue
+        q.put((rank, repr(ex)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("D,k", [(8, 2), (9, 3)])
+def test_two_rank_evalpoint_exchange(D, k):
+    # the all-to-all of the evaluation-point variant (north_star (4)): after the exchange each
+    # rank holds every point's values on exactly its own columns
+    import paper_1608_00206_b200.build as b
+    b.build()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ep_worker, args=(r, world, port, D, k, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok is True for _, ok in res), res
