@@ -213,6 +213,15 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of oracle work per reference step")
+    ap.add_argument("--variant", default="split", choices=["split", "evalpoint"],
+                    help="multi-GPU scheme: 'split' = zero-communication output split (default); "
+                         "'evalpoint' = top-axis evaluation points per rank + all-to-all + top inverse "
+                         "(BASELINE north_star (4))")
+    ap.add_argument("--ep-k", type=int, default=4, help="top axes of the evalpoint variant")
+    ap.add_argument("--vshards", type=int, default=8,
+                    help="c5 (D=22, 251 GB of output): the output is computed as this many shards of the "
+                         "zero-communication split, streamed through one reused device buffer; rank r of N "
+                         "runs shards [r*V/N, (r+1)*V/N)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets several ranks share one GPU (testing the N > 1 path on one device)")
     args = ap.parse_args()
@@ -244,6 +253,7 @@ def main():
     w = WORKLOADS[wl]
     D = w["D"]
     batched = "B" in w
+    plan = None
     x_np, y_np = hcgen.config_inputs(w["cfg"])
     tdt = torch.float64 if x_np.dtype == np.float64 else torch.int64
     xg = torch.from_numpy(x_np).cuda()
@@ -262,6 +272,38 @@ def main():
             hc.convolve_batched(xg, yg, z)
         in_bytes = 2 * B * 2 ** D * 8
         prof_name = "tile"
+    elif args.variant == "evalpoint":
+        ep = hc.EPPlan(D, args.ep_k, str(x_np.dtype), world, rank)
+        nc = 3 ** (D - args.ep_k)
+        w_ep = torch.empty((ep.e1 - ep.e0) * nc, dtype=tdt, device="cuda")
+        wt = torch.empty(3 ** args.ep_k * (ep.c1 - ep.c0), dtype=tdt, device="cuda")
+        z = torch.empty_like(wt)
+        n_local = z.numel()
+        n_total = 3 ** D
+        xdist = dist if world > 1 else None
+
+        def step():
+            ep.local(xg, yg, w_ep)
+            hc.ep_exchange(w_ep, wt, D, args.ep_k, rank, world, xdist)
+            ep.finish(wt, z)
+        in_bytes = 2 * 2 ** D * 8
+        prof_name = "slab"
+        plan = None
+    elif wl == "c5_d22_f64":
+        V = args.vshards
+        if V % world != 0:
+            raise SystemExit("--vshards must be a multiple of the number of ranks")
+        vplans = [hc.Plan(D, str(x_np.dtype), V, s) for s in range(rank * V // world, (rank + 1) * V // world)]
+        sizes = [e - b for b, e in (p.shard_info() for p in vplans)]
+        zbuf = torch.empty(max(sizes), dtype=tdt, device="cuda")
+        n_local = sum(sizes)
+        n_total = 3 ** D
+
+        def step():
+            for p, m in zip(vplans, sizes):
+                p.convolve_sharded(xg, yg, zbuf[:m])
+        in_bytes = 2 * 2 ** D * 8
+        prof_name = "slab"
     else:
         plan = hc.Plan(D, str(x_np.dtype), world, rank)
         zb, ze = plan.shard_info()
@@ -317,7 +359,7 @@ def main():
     launches_per_step = kcount / max(args.steps, 1)
     out_bytes_local = n_local * 8
     in_bytes_local = in_bytes if not batched else in_bytes
-    alg_bytes_per_launch = (out_bytes_local + in_bytes_local * (1 if batched else 1)) / max(launches_per_step, 1)
+    alg_bytes_per_launch = (out_bytes_local + in_bytes_local * max(launches_per_step, 1)) / max(launches_per_step, 1)
     peak, peak_src = load_peaks()
     achieved = alg_bytes_per_launch / (k_avg / 1e3) / 1e9 if k_avg > 0 else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -327,7 +369,7 @@ def main():
 
     # end to end through the host-buffer C-ABI entry point (pinned host memory, copies inside)
     e2e = None
-    if not args.no_e2e and not batched:
+    if not args.no_e2e and not batched and plan is not None:
         xh = torch.from_numpy(x_np).pin_memory()
         yh = torch.from_numpy(y_np).pin_memory()
         zh = torch.empty(n_local, dtype=tdt).pin_memory()
@@ -357,8 +399,11 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64" if tdt == torch.float64 else "int64",
             "data": "synthetic",
-            "config": {"workload": wl, "desc": w["desc"], "D": D, "output_entries": n_total,
-                       "parallelism": f"output-split x{world}" if world > 1 else "single",
+            "config": {"workload": wl, "desc": w["desc"], "D": D, "output_entries": n_total, "variant": args.variant,
+                       "parallelism": (f"evalpoint k={args.ep_k} x{world} (all-to-all)" if args.variant == "evalpoint"
+                                       else (f"{args.vshards} output-split shards streamed through one buffer, "
+                                             f"{args.vshards // world} per rank x{world}" if wl == "c5_d22_f64"
+                                             else (f"output-split x{world}" if world > 1 else "single"))),
                        "l2": "output (%.1f GB) > L2 (126 MB): every step streams the whole output" % (n_total * 8 / 1e9),
                        "min_bytes_per_step": n_total * 8 + in_bytes},
             "hbm_gbs_min_bytes": (n_total * 8 + in_bytes) / (ms_per_step / 1e3) / 1e9,
