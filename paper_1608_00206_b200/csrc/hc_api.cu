@@ -17,6 +17,7 @@
 #include "hc_common.cuh"
 #include "hc_tile.cuh"
 #include "hc_slab.cuh"
+#include "hc_ws.cuh"
 
 using namespace hc;
 
@@ -179,8 +180,48 @@ cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const Sla
   return cudaGetLastError();
 }
 
+// warp-specialised variant (hc_ws.cuh): one CTA per SM
+template <class T, int M>
+cudaError_t launch_slabws_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st) {
+  auto kern = slabws_kernel<T, M>;
+  static int grid_max = 0;
+  if (!grid_max) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSCfg<T, M>::SMEM);
+    if (e != cudaSuccess) return e;
+    int occ = 0, dev = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WS_NT, WSCfg<T, M>::SMEM);
+    if (e != cudaSuccess) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    grid_max = occ * sms;
+  }
+  const uint64_t tiles = (uint64_t)a.nslab * upow3(M);
+  const unsigned grid = (unsigned)(tiles < (uint64_t)grid_max ? tiles : (uint64_t)grid_max);
+  cudaError_t e = cudaMemsetAsync(a.ctr, 0, sizeof(uint32_t) * (2 + 2 * (size_t)a.nslab), st);
+  if (e != cudaSuccess) return e;
+  {
+    LaunchScope lp("prep", st);
+    dim3 pg((unsigned)upow3(M), 1u << a.k, 2);
+    prep_kernel<T, M><<<pg, 256, 0, st>>>(x, y, xu, yu);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  LaunchScope ls("slab", st);
+  kern<<<grid, WS_NT, WSCfg<T, M>::SMEM, st>>>(xu, yu, z, a);
+  return cudaGetLastError();
+}
+
 template <class T>
 cudaError_t launch_slab8(const T* x, const T* y, T* z, T* xu, T* yu, int M, const SlabArgs& a, cudaStream_t st) {
+  static const int ws = getenv("HC_SLAB_WS") ? atoi(getenv("HC_SLAB_WS")) : 0;
+  if (ws) {
+    switch (M) {
+      case 5: return launch_slabws_m<T, 5>(x, y, z, xu, yu, a, st);
+      case 6: return launch_slabws_m<T, 6>(x, y, z, xu, yu, a, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (M) {
     case 5: return launch_slab8_m<T, 5>(x, y, z, xu, yu, a, st);
     case 6: return launch_slab8_m<T, 6>(x, y, z, xu, yu, a, st);
@@ -346,7 +387,7 @@ extern "C" hc_status hc_plan_create(hc_plan_t* out, int D, hc_dtype dtype, int n
   p->cuts = compute_cuts(g.k, ngpu);
   {
     for (auto& c : p->ctr) {
-      if (cudaMalloc(&c, sizeof(uint32_t) * (1 + g.nunits)) != cudaSuccess) {
+      if (cudaMalloc(&c, sizeof(uint32_t) * (2 + 2 * g.nunits)) != cudaSuccess) {
         cudaGetLastError();
         for (auto& c2 : p->ctr) cudaFree(c2);
         delete p;
@@ -455,6 +496,11 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
       cudaStreamSynchronize(st);
       double tot = 0;
       for (int i = 0; i < 7; ++i) tot += (double)h[i];
+      if (getenv("HC_SLAB_WS") && atoi(getenv("HC_SLAB_WS")))
+        fprintf(stderr, "ws phase (Mclk, CTA sum): compute: throttle %.0f pairloop %.0f S-wait %.0f handoff %.0f | "
+                "epilogue: tiles %.0f p2 %.0f idle %.0f\n", h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6,
+                h[4] / 1e6, h[5] / 1e6, h[6] / 1e6);
+      else
       fprintf(stderr, "phase(Mclk/CTA-sum): select+wait %.0f pairloop %.0f inv+store %.0f p2 %.0f end %.0f "
               "(tot %.0f) | F1 mbar wait %.0f\n", h[0] / 1e6, h[1] / 1e6, h[6] / 1e6, h[4] / 1e6, h[5] / 1e6,
               tot / 1e6, h[7] / 1e6);

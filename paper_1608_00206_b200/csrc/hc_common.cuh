@@ -66,47 +66,6 @@ __device__ __forceinline__ void fwd_mul_acc(const T* x, const T* y, T* acc) {
   }
 }
 
-// acc[k] += sum_{i + j = k} x[i] y[j] over N axes by the paper's direct 4-way split
-// (PAPER.md 166-177) on every axis: 4^N fused multiply-adds, no forward adds and no
-// inverse.  Index k = sum_b k_b 3^b, i, j = sum_b i_b 2^b; pairs in ascending (i, j).
-template <int N, class T>
-__device__ __forceinline__ void direct_mul_acc(const T* x, const T* y, T* acc) {
-#pragma unroll
-  for (int i = 0; i < (1 << N); ++i) {
-#pragma unroll
-    for (int j = 0; j < (1 << N); ++j) {
-      int k = 0, p3 = 1;
-#pragma unroll
-      for (int b = 0; b < N; ++b) {
-        k += (((i >> b) & 1) + ((j >> b) & 1)) * p3;
-        p3 *= 3;
-      }
-      acc[k] = Ar<T>::mad(x[i], y[j], acc[k]);
-    }
-  }
-}
-
-// Register-cube product for the tile's 3 register axes: Karatsuba (PAPER.md 185-192) on the
-// top axis, the direct split on the two lower ones.  On an FMA machine a forward add costs
-// as much as the multiply it saves, so this mix needs 3 x 16 FMA + 8 adds = 56 operations
-// per pair against 65 for Karatsuba on all three axes (and 64 for direct on all three); only
-// the top axis then needs the inverse (inv_top3).
-template <class T>
-__device__ __forceinline__ void kdd_mul_acc(const T* x, const T* y, T* acc) {
-  direct_mul_acc<2, T>(x, y, acc);              // e_top = 0: x0 * y0
-  direct_mul_acc<2, T>(x + 4, y + 4, acc + 18);  // e_top = 2: x1 * y1
-  T xs[4], ys[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) { xs[i] = Ar<T>::add(x[i], x[i + 4]); ys[i] = Ar<T>::add(y[i], y[i + 4]); }
-  direct_mul_acc<2, T>(xs, ys, acc + 9);         // e_top = 1: (x0 + x1) * (y0 + y1)
-}
-// inverse on the top register axis only: (c0, c1, c2) -> (c0, (c1 - c0) - c2, c2)
-template <class T>
-__device__ __forceinline__ void inv_top3(T* a) {
-#pragma unroll
-  for (int i = 0; i < 9; ++i) a[9 + i] = Ar<T>::sub(Ar<T>::sub(a[9 + i], a[i]), a[18 + i]);
-}
-
 // In-place inverse 3^N -> 3^N over all N axes: (c0, c1, c2) -> (c0, (c1 - c0) - c2, c2).
 template <int N, int AX, class T>
 __device__ __forceinline__ void inv_axis(T* a) {

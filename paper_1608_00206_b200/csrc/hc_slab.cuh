@@ -7,8 +7,7 @@
 // axes; the paper's 4-way split (PAPER.md 166-177) on the k top axes (pair-sum).
 //
 // Tile axes (bit / trit b of the tile index, b = 0 fastest):
-//   C = {0,1,2}  register axes: 27 accumulators per thread (Karatsuba on axis 2, the direct
-//                split on axes 0, 1: see kdd_mul_acc)
+//   C = {0,1,2}  register axes: 27 accumulators per thread
 //   B = {3,4,5}  evaluated by the F1 warps, in registers
 //   a1 = 6       evaluated by the F1 warps (one warp per evaluation point e_a1)
 //   a2 = 7       summed by the F2 threads while they load (e_a2 = 1: two rows)
@@ -234,10 +233,11 @@ __device__ __forceinline__ void t8_f2(const T* P, int ea2, int eS, T* acc) {
       yt[j + 1] = Ar<T>::add(yt[j + 1], v1);
     }
   }
-  // fp64: FMA-bound, the Karatsuba/direct mix is cheaper; uint64: a 64-bit multiply costs
-  // several integer instructions, so Karatsuba on all three axes stays cheaper
-  if constexpr (sizeof(T) == 8 && T(0.5) != T(0)) kdd_mul_acc<T>(xt, yt, acc);
-  else fwd_mul_acc<3, T>(xt, yt, acc);
+  // Karatsuba on all three register axes.  (The direct split on the lower two needs fewer
+  // operations -- 48 FMA + 8 adds against 27 + 38 -- but a DFMA with three register operands
+  // issues at ~2.8 clk per warp and SM sub-partition against ~1.1 for DADD on this B200, so
+  // it is slower: tools/microbench/mb6.cu, profiles/r01_smem_microbench.txt.)
+  fwd_mul_acc<3, T>(xt, yt, acc);
 }
 
 // Prefetch cursor (shared memory, thread 0 only) over the pairs of the pass-1 items in the
@@ -313,8 +313,7 @@ __device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, Raw
   // Unit u = (e_A, e_B) with e_A = e_a1 + 3 e_a2, so S[e_A][e_B][k_C] = S[27 u + k_C]
   // (stride 27: conflict-free whatever the thread-to-unit map).
   if (unit) {
-    if constexpr (T(0.5) != T(0)) inv_top3<T>(acc);  // fp64: the lower register axes were direct
-    else inv_reg<3, T>(acc);
+    inv_reg<3, T>(acc);
 #pragma unroll
     for (int i = 0; i < 27; ++i) S[u * 27 + i] = acc[i];
   }
@@ -603,7 +602,8 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       // barrier): the reads below are ordered after it by that control dependency and the
       // barrier, and go to L2 (.cg), where the producers' fenced stores already are
       if (threadIdx.x == T8_SCHED) pump();
-      p2_item<T, M, 8>(zs, it.r, sm, threadIdx.x < 243 ? (int)threadIdx.x : -1, T8_SCHED, signal);
+      p2_item<T, M, 8>(zs, it.r, sm, threadIdx.x < 243 ? (int)threadIdx.x : -1, T8_SCHED, signal,
+                       [] { __syncthreads(); });
       PH_MARK(4);
     }
     __syncthreads();  // the item's smem is free

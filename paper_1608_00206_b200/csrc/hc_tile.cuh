@@ -303,8 +303,9 @@ struct P2Cfg {
   static constexpr int P2S = NLO * P2W + ((9 - NLO * P2W) % 16 + 16) % 16;
   static constexpr int SIZE = NHI * P2S;
 };
-template <class T, int M, int L, class Mid>
-__device__ __forceinline__ void p2_item(T* __restrict__ zs, uint32_t c, T* sm, int task, int sched, Mid&& mid) {
+template <class T, int M, int L, class Mid, class Bar>
+__device__ __forceinline__ void p2_item(T* __restrict__ zs, uint32_t c, T* sm, int task, int sched, Mid&& mid,
+                                        Bar&& bar) {
   // task in [0, 243) or -1 (idle lane); 243 = 3^5 task slots per round
   using Q = P2Cfg<M>;
   constexpr int LO = Q::LO, HI = Q::HI, NLO = Q::NLO, NHI = Q::NHI, P2S = Q::P2S;
@@ -321,7 +322,7 @@ __device__ __forceinline__ void p2_item(T* __restrict__ zs, uint32_t c, T* sm, i
 #pragma unroll
       for (int e = 0; e < NLO; ++e) sm[eh * P2S + e * P2W + pos] = v[e];
     }
-  __syncthreads();
+  bar();
   if ((int)threadIdx.x == sched) mid();  // between the loads and the stores (see slab8_kernel)
   // round 2: task (e_lo, pos) interpolates over HI axes and stores the final values
   if (task >= 0)

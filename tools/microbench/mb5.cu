@@ -24,8 +24,16 @@ __global__ void __launch_bounds__(T8_NT, 2) k_pairs(int iters, double* sink) {
   for (int i = 0; i < 27; ++i) acc[i] = 0;
   for (int p = 0; p < iters; ++p) {
     if (MODE != 1 && t8_f1_es(w) >= 0) t8_f1<double>(R + (p % T8_NRAW) * RS_SZ, P + ((p + 1) & 1) * PS_SZ, t8_f1_es(w), lane);
-    if (MODE != 2 && unit) t8_f2<double>(P + (p & 1) * PS_SZ, ea2, eS, acc);
-    if (MODE != 3) __syncthreads();
+    if (MODE == 4 && unit) {  // F2 arithmetic only: inputs from registers (no shared loads)
+      double xt[8], yt[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // vary the low mantissa bits only (integer pipe)
+        xt[j] = __longlong_as_double(0x3f50624dd2f1a9fcll ^ (long long)((p + j) & 255));
+        yt[j] = __longlong_as_double(0x3f60624dd2f1a9fcll ^ (long long)((p * 3 + j) & 255));
+      }
+      fwd_mul_acc<3, double>(xt, yt, acc);
+    } else if (MODE != 2 && unit) t8_f2<double>(P + (p & 1) * PS_SZ, ea2, eS, acc);
+    if (MODE != 3 && MODE != 4) __syncthreads();
   }
   double s = 0;
 #pragma unroll
@@ -57,12 +65,12 @@ int main() {
   double* sink;
   cudaMalloc(&sink, 8);
   const int iters = 20000;
-  const char* names[] = {"F1+F2+bar", "F2+bar", "F1+bar", "F1+F2 nobar"};
+  const char* names[] = {"F1+F2+bar", "F2+bar", "F1+bar", "F1+F2 nobar", "F2 math only"};
   for (int ctas = 1; ctas <= 2; ++ctas) {
     const int grid = sms * ctas;
-    for (int m = 0; m < 4; ++m) {
+    for (int m = 0; m < 5; ++m) {
       float ms = m == 0 ? run<0>(grid, iters, sink) : m == 1 ? run<1>(grid, iters, sink)
-               : m == 2 ? run<2>(grid, iters, sink) : run<3>(grid, iters, sink);
+               : m == 2 ? run<2>(grid, iters, sink) : m == 3 ? run<3>(grid, iters, sink) : run<4>(grid, iters, sink);
       // clk per pair iteration per SM (all CTAs on the SM together)
       const double clk_per = (ms * 1e-3) * (clk * 1e3) / ((double)iters * ctas);
       printf("ctas/SM %d %-12s %.3f ms  %.0f clk per pair-iteration per SM\n", ctas, names[m], ms, clk_per);
