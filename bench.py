@@ -39,7 +39,23 @@ WORKLOADS = {
     "c5_d22_f64": dict(cfg="c5_d22_f64", D=22, desc="single pair D=22 fp64 Exp(1)-normalized, sharded (BASELINE config 5)"),
     "c2_b65536_d8_i64": dict(cfg="c2_b65536_d8_i64", D=8, B=65536,
                              desc="65536 independent pairs D=8 int64 uniform [0,255] (BASELINE config 2)"),
+    # SURVEY.md §8(f) rows, on config-4-sized inputs (D = 20)
+    "f1_conv1d_d20_i64": dict(cfg="c3_like_d20_i64", D=20, app="conv1d",
+                              desc="f1: ordinary 1-D convolution of two length-2^20 int64 vectors (uniform [0,2^16)) "
+                                   "= carry-free hypercube convolution + carries"),
+    "f2_maxconv_d20_f64": dict(cfg="c4_d20_f64", D=20, app="maxconv",
+                               desc="f2: p-norm max-convolution (p = 16) of the config-4 inputs"),
+    "f4_difference_d20_f64": dict(cfg="c4_d20_f64", D=20, app="difference",
+                                  desc="f4: PMF of X - Y for the config-4 Bernoulli-axis PMFs"),
 }
+
+
+def workload_inputs(w):
+    """Seeded synthetic inputs of a workload (hcgen): BASELINE configs, or the f1 row's vectors."""
+    if w["cfg"] == "c3_like_d20_i64":
+        return (hcgen.uniform_int(1020, 0, 1 << 20, 0, (1 << 16) - 1),
+                hcgen.uniform_int(1020, 1, 1 << 20, 0, (1 << 16) - 1))
+    return hcgen.config_inputs(w["cfg"])
 
 
 def load_peaks():
@@ -143,7 +159,7 @@ def oracle_sample_rate(wl, budget_s=10.0, seed=99):
     D = w["D"]
     cores = oracle.max_threads()
     if "B" in w:
-        x, y = hcgen.config_inputs(w["cfg"])
+        x, y = workload_inputs(w)
         rng = np.random.default_rng(seed)
         nb = 256
         bs = rng.choice(x.shape[0], size=nb, replace=False)
@@ -152,7 +168,7 @@ def oracle_sample_rate(wl, budget_s=10.0, seed=99):
         dt = time.perf_counter() - t0
         n = nb * 3 ** D
         return n / dt, cores, f"{nb} of {x.shape[0]} cubes, full Algorithm 1 each ({n} entries)", dt
-    x, y = hcgen.config_inputs(w["cfg"])
+    x, y = workload_inputs(w)
     rng = np.random.default_rng(seed)
     m = 3 ** D
     n = 20000
@@ -254,7 +270,7 @@ def main():
     D = w["D"]
     batched = "B" in w
     plan = None
-    x_np, y_np = hcgen.config_inputs(w["cfg"])
+    x_np, y_np = workload_inputs(w)
     tdt = torch.float64 if x_np.dtype == np.float64 else torch.int64
     xg = torch.from_numpy(x_np).cuda()
     yg = torch.from_numpy(y_np).cuda()
@@ -272,6 +288,28 @@ def main():
             hc.convolve_batched(xg, yg, z)
         in_bytes = 2 * B * 2 ** D * 8
         prof_name = "tile"
+    elif "app" in w:
+        if world > 1:
+            raise SystemExit("application workloads are single-GPU in this bench")
+        app_plan = hc.Plan(D, str(x_np.dtype))
+        z = torch.empty(3 ** D, dtype=tdt, device="cuda")
+        n_local = n_total = 3 ** D
+        if w["app"] == "conv1d":
+            out1 = torch.empty((2 << D) - 1, dtype=tdt, device="cuda")
+            work = torch.empty(hc.carries_work_len(D), dtype=tdt, device="cuda")
+
+            def step():
+                app_plan.convolve(xg, yg, z)
+                hc.apply_carries(D, z, out1, work)
+        elif w["app"] == "maxconv":
+            def step():
+                app_plan.maxconv_pnorm(xg, yg, z, 16.0)
+        else:
+            def step():
+                app_plan.convolve_difference(xg, yg, z)
+        in_bytes = 2 * 2 ** D * 8
+        prof_name = "slab"
+        plan = None  # no host-buffer e2e for the application rows
     elif args.variant == "evalpoint":
         ep = hc.EPPlan(D, args.ep_k, str(x_np.dtype), world, rank)
         nc = 3 ** (D - args.ep_k)
@@ -399,7 +437,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64" if tdt == torch.float64 else "int64",
             "data": "synthetic",
-            "config": {"workload": wl, "desc": w["desc"], "D": D, "output_entries": n_total, "variant": args.variant,
+            "config": {"workload": wl, "desc": w["desc"], "D": D, "output_entries": n_total,
+                       "variant": w.get("app", args.variant),
                        "parallelism": (f"evalpoint k={args.ep_k} x{world} (all-to-all)" if args.variant == "evalpoint"
                                        else (f"{args.vshards} output-split shards streamed through one buffer, "
                                              f"{args.vshards // world} per rank x{world}" if wl == "c5_d22_f64"

@@ -132,6 +132,33 @@ hc_status hc_ep_local(hc_ep_t p, const void* x, const void* y, void* w, void* st
  * ncols = col_end - col_begin; z must not alias wt. */
 hc_status hc_ep_finish(hc_ep_t p, const void* wt, void* z, void* stream);
 
+/* ---- Applications built on the hot path ------------------------------ */
+
+/* f4: PMF of the difference X - Y of independent random vectors with Bernoulli axes
+ * (PAPER.md 35-38, 147-149).  x[i] = P(X = i), y[j] = P(Y = j) (2^D each); z (3^D) receives
+ * z[k] = P(X - Y = d) with d_b = k_b - 1 in {-1, 0, 1}, k = sum_b k_b 3^b.  Computed as
+ * conv(x, flip(y)), flip(y)[j] = y[~j] (per-axis complement: X - Y + 1 = X + (1 - Y)); the
+ * plan keeps flip(y) in its own scratch (2^D elements).  Whole output (like hc_convolve). */
+hc_status hc_convolve_difference(hc_plan_t plan, const void* x, const void* y, void* z, void* stream);
+
+/* f1: carries -- turns the carry-free convolution (the hot path on two length-2^D vectors,
+ * bit b of an index = axis b; PAPER.md 354-373) into the ordinary 1-D convolution:
+ *     out[m] = sum_{k : sum_b k_b 2^b = m} z[k],   m in [0, 2^(D+1) - 1).
+ * z: 3^D elements (device), out: 2^(D+1) - 1 elements (device), work: hc_carries_work_len(D)
+ * elements of the same type (device; may be NULL when that is 0).  Stream-ordered. */
+uint64_t hc_carries_work_len(int D);
+hc_status hc_apply_carries(int D, hc_dtype dtype, const void* z, void* out, void* work, void* stream);
+
+/* f2: p-norm max-convolution (PAPER.md 341-352), fp64 plans only.  x, y >= 0 (2^D each):
+ *     z[k] = mx * my * ( sum_{i+j=k} (x[i]/mx)^p (y[j]/my)^p )^(1/p),   mx = max x, my = max y,
+ * which lies in [M, n_k^(1/p) M] for the max-convolution M = max_{i+j=k} x[i] y[j] and the
+ * n_k = 2^{#1(k)} terms of cell k (relative error <= 1 - n_k^(-1/p)).  round_to_int != 0
+ * rounds z to the nearest integer: exact for integer inputs whenever M (2^D)^(1/p) - M < 0.5
+ * over all cells (the paper's bounded-range criterion) and no nonzero term underflows.
+ * p >= 1.  The plan keeps the scaled powers in its scratch (2 x 2^D elements). */
+hc_status hc_maxconv_pnorm(hc_plan_t plan, const void* x, const void* y, void* z, double p, int round_to_int,
+                           void* stream);
+
 /* Instrumentation (for bench.py / tests): cumulative number of kernels this library has
  * launched in this process, and per-kernel device time when profiling is enabled
  * (events recorded around each launch on the launching stream). */

@@ -324,6 +324,10 @@ struct hc_plan_s {
   void* dz[2] = {nullptr, nullptr};
   uint64_t chunk_units = 0;
   cudaStream_t hs[2] = {nullptr, nullptr};
+  // application scratch (hc_convolve_difference, hc_maxconv_pnorm): 2 x 2^D elements + maxima
+  void* app_a = nullptr;
+  void* app_b = nullptr;
+  unsigned long long* app_mx = nullptr;
 };
 
 // Equal-cost contiguous split of the 3^k output slabs over ngpu ranks.  Cost of slab
@@ -416,6 +420,9 @@ extern "C" hc_status hc_plan_destroy(hc_plan_t p) {
   for (auto& c : p->ctr) cudaFree(c);
   cudaFree(p->xu);
   cudaFree(p->yu);
+  cudaFree(p->app_a);
+  cudaFree(p->app_b);
+  cudaFree(p->app_mx);
   for (auto& kv : p->orders) cudaFree(kv.second);
   for (auto& s : p->hs)
     if (s) cudaStreamDestroy(s);
@@ -698,4 +705,136 @@ extern "C" hc_status hc_ep_finish(hc_ep_t p, const void* wt, void* z, void* stre
                       ? ep_finish_t<uint64_t>(p, (const uint64_t*)wt, (uint64_t*)z, (cudaStream_t)stream)
                       : ep_finish_t<double>(p, (const double*)wt, (double*)z, (cudaStream_t)stream);
   return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------------------------------
+// Applications (include/hc.h; kernels in hc_apps.cuh)
+#include "hc_apps.cuh"
+
+namespace {
+hc_status app_scratch(hc_plan_t p) {
+  if (p->app_a) return HC_OK;
+  const size_t bytes = sizeof(double) << p->D;
+  if (cudaMalloc(&p->app_a, bytes) != cudaSuccess || cudaMalloc(&p->app_b, bytes) != cudaSuccess ||
+      cudaMalloc(&p->app_mx, 2 * sizeof(unsigned long long)) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(p->app_a);
+    cudaFree(p->app_b);
+    cudaFree(p->app_mx);
+    p->app_a = p->app_b = nullptr;
+    p->app_mx = nullptr;
+    return HC_ERR_CAPACITY;
+  }
+  return HC_OK;
+}
+unsigned ew_grid(uint64_t n) {
+  const uint64_t g = (n + 255) / 256;
+  return (unsigned)(g < 148 * 16 ? (g ? g : 1) : 148 * 16);
+}
+template <class T, int L>
+cudaError_t carry_tile(const T* z, T* part, uint64_t ntiles, cudaStream_t st) {
+  const size_t sm = 2 * sizeof(T) * (size_t)ipow3(L);
+  auto k = carry_tile_kernel<T, L>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  LaunchScope ls("carry", st);
+  k<<<(unsigned)ntiles, 256, sm, st>>>(z, part);
+  return cudaGetLastError();
+}
+template <class T>
+cudaError_t apply_carries_t(int D, const T* z, T* out, T* work, cudaStream_t st) {
+  const int L = D < 8 ? D : 8;
+  const uint64_t ntiles = upow3(D - L);
+  T* part = D == L ? out : work;
+  cudaError_t e;
+  switch (L) {
+    case 1: e = carry_tile<T, 1>(z, part, ntiles, st); break;
+    case 2: e = carry_tile<T, 2>(z, part, ntiles, st); break;
+    case 3: e = carry_tile<T, 3>(z, part, ntiles, st); break;
+    case 4: e = carry_tile<T, 4>(z, part, ntiles, st); break;
+    case 5: e = carry_tile<T, 5>(z, part, ntiles, st); break;
+    case 6: e = carry_tile<T, 6>(z, part, ntiles, st); break;
+    case 7: e = carry_tile<T, 7>(z, part, ntiles, st); break;
+    default: e = carry_tile<T, 8>(z, part, ntiles, st); break;
+  }
+  if (e != cudaSuccess) return e;
+  // remaining axes c = L .. D-1 in global memory, ping-pong in `work`
+  const uint64_t half = D > 8 ? upow3(D - 8) * 511 : 0;
+  T* A = part;
+  uint64_t nr = ntiles;
+  for (int c = L; c < D; ++c) {
+    const uint64_t nr2 = nr / 3;
+    T* B = (c + 1 == D) ? out : (A == work ? work + half : work);
+    const uint64_t n2 = nr2 * ((4ull << c) - 1);
+    LaunchScope ls("carry", st);
+    if (n2 < (1ull << 32)) carry_step_kernel<T, uint32_t><<<ew_grid(n2), 256, 0, st>>>(A, B, nr2, c);
+    else carry_step_kernel<T, uint64_t><<<ew_grid(n2), 256, 0, st>>>(A, B, nr2, c);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    A = B;
+    nr = nr2;
+  }
+  return cudaSuccess;
+}
+}  // namespace
+
+extern "C" uint64_t hc_carries_work_len(int D) {
+  if (D < 1 || D > HC_MAX_D) return 0;
+  return D <= 8 ? 0 : 2 * upow3(D - 8) * 511;
+}
+
+extern "C" hc_status hc_apply_carries(int D, hc_dtype dtype, const void* z, void* out, void* work, void* stream) {
+  if (D < 1 || D > HC_MAX_D) return HC_ERR_INVALID_DIM;
+  if (dtype != HC_INT64 && dtype != HC_FP64) return HC_ERR_DTYPE;
+  if (!z || !out || (D > 8 && !work)) return HC_ERR_NULL;
+  hc_status ds = check_device();
+  if (ds != HC_OK) return ds;
+  cudaError_t e = dtype == HC_INT64
+                      ? apply_carries_t<uint64_t>(D, (const uint64_t*)z, (uint64_t*)out, (uint64_t*)work, (cudaStream_t)stream)
+                      : apply_carries_t<double>(D, (const double*)z, (double*)out, (double*)work, (cudaStream_t)stream);
+  return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
+}
+
+extern "C" hc_status hc_convolve_difference(hc_plan_t p, const void* x, const void* y, void* z, void* stream) {
+  if (!p || !x || !y || !z) return HC_ERR_NULL;
+  if (!aligned16(x) || !aligned16(y) || !aligned8(z)) return HC_ERR_ALIGN;
+  hc_status s = app_scratch(p);
+  if (s != HC_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    LaunchScope ls("flip", st);
+    if (p->dtype == HC_INT64) flip_kernel<uint64_t><<<ew_grid(1ull << p->D), 256, 0, st>>>((const uint64_t*)y, (uint64_t*)p->app_a, p->D);
+    else flip_kernel<double><<<ew_grid(1ull << p->D), 256, 0, st>>>((const double*)y, (double*)p->app_a, p->D);
+    if (cudaGetLastError() != cudaSuccess) return HC_ERR_CUDA;
+  }
+  return run_range(p, x, p->app_a, z, 0, p->g.nunits, st, 0);
+}
+
+extern "C" hc_status hc_maxconv_pnorm(hc_plan_t p, const void* x, const void* y, void* z, double pw, int round_to_int,
+                                      void* stream) {
+  if (!p || !x || !y || !z) return HC_ERR_NULL;
+  if (p->dtype != HC_FP64) return HC_ERR_DTYPE;
+  if (!(pw >= 1.0)) return HC_ERR_INVALID_DIM;
+  if (!aligned16(x) || !aligned16(y) || !aligned8(z)) return HC_ERR_ALIGN;
+  hc_status s = app_scratch(p);
+  if (s != HC_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t n = 1ull << p->D;
+  int sq = -1;  // p = 2^sq: powers by squaring and roots by square roots (exact shape of the paper's p)
+  for (int k = 0; k < 11; ++k)
+    if (pw == (double)(1 << k)) sq = k;
+  if (cudaMemsetAsync(p->app_mx, 0, 2 * sizeof(unsigned long long), st) != cudaSuccess) return HC_ERR_CUDA;
+  {
+    LaunchScope ls("pnorm_pre", st);
+    max_nonneg_kernel<<<ew_grid(n), 256, 0, st>>>((const double*)x, n, p->app_mx);
+    max_nonneg_kernel<<<ew_grid(n), 256, 0, st>>>((const double*)y, n, p->app_mx + 1);
+    pnorm_pre_kernel<<<ew_grid(n), 256, 0, st>>>((const double*)x, (double*)p->app_a, n, pw, sq, p->app_mx);
+    pnorm_pre_kernel<<<ew_grid(n), 256, 0, st>>>((const double*)y, (double*)p->app_b, n, pw, sq, p->app_mx + 1);
+    if (cudaGetLastError() != cudaSuccess) return HC_ERR_CUDA;
+  }
+  s = run_range(p, p->app_a, p->app_b, z, 0, p->g.nunits, st, 0);
+  if (s != HC_OK) return s;
+  LaunchScope ls("pnorm_post", st);
+  pnorm_post_kernel<<<ew_grid(upow3(p->D)), 256, 0, st>>>((double*)z, upow3(p->D), pw, sq, p->app_mx, round_to_int);
+  return cudaGetLastError() == cudaSuccess ? HC_OK : HC_ERR_CUDA;
 }

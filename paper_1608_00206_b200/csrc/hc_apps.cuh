@@ -1,0 +1,133 @@
+// hc_apps.cuh -- kernels of the applications built on the hot path;
+// C ABI in include/hc.h (hc_convolve_difference, hc_apply_carries, hc_maxconv_pnorm).
+//
+//  f4  PMF of differences of Bernoulli-axis random vectors (PAPER.md 35-38, 147-149):
+//      P(X - Y = d) = sum_{i - j = d} x[i] y[j] = conv(x, flip(y))[d + 1], flip(y)[j] =
+//      y[~j]: the per-axis complement turns a difference into a sum (flip_kernel).
+//  f1  carry-free convolution -> ordinary 1-D convolution (PAPER.md 354-373): the hot path
+//      is the carry-free convolution of two length-2^D vectors (bit b = axis b); the carries
+//      are out[m] = sum_{k : sum_b k_b 2^b = m} z[k], done axis by axis -- after the low c
+//      axes are combined a row holds the values v = sum_{b<c} k_b 2^b in [0, 2^(c+1) - 1),
+//      and combining axis c is  B[r][v'] = sum_{k_c} A[k_c + 3 r][v' - k_c 2^c].
+//      carry_tile_kernel does the low min(D, 8) axes of one 3^8 tile in shared memory;
+//      carry_step_kernel does one further axis in global memory.
+//  f2  p-norm max-convolution (PAPER.md 341-352): max_{i+j=k} x[i] y[j] ~
+//      (sum_{i+j=k} x[i]^p y[j]^p)^(1/p) = (x^p * y^p)[k]^(1/p); inputs are scaled by their
+//      maxima first so the powers stay in range (pnorm_pre_kernel / pnorm_post_kernel).
+#pragma once
+#include "hc_common.cuh"
+
+namespace hc {
+
+// f4 -----------------------------------------------------------------------------------
+template <class T>
+__global__ void __launch_bounds__(256) flip_kernel(const T* __restrict__ y, T* __restrict__ yf, int D) {
+  const uint64_t n = 1ull << D;
+  const uint64_t mask = n - 1;
+  for (uint64_t j = (uint64_t)blockIdx.x * 256 + threadIdx.x; j < n; j += (uint64_t)gridDim.x * 256)
+    yf[j] = y[~j & mask];
+}
+
+// f1 -----------------------------------------------------------------------------------
+// One combining step on rows: A is [nr_in][V], V = 2^(c+1) - 1; B is [nr_in / 3][2^(c+2) - 1].
+template <class T, class I>
+__device__ __forceinline__ T carry_gather(const T* A, I V, I r, I v, int c) {
+  T s = T(0);
+#pragma unroll
+  for (int kc = 0; kc < 3; ++kc) {
+    const I off = (I)kc << c;
+    if (v >= off && v - off < V) s = Ar<T>::add(s, A[(uint64_t)(kc + 3 * r) * V + (v - off)]);
+  }
+  return s;
+}
+
+// tile of the low L = min(D, 8) axes (3^L values of z) -> 2^(L+1) - 1 partial sums, combining
+// axis 0, 1, ..., L-1 in shared memory; grid = 3^(D-L) tiles, block 256
+template <class T, int L>
+__global__ void __launch_bounds__(256) carry_tile_kernel(const T* __restrict__ z, T* __restrict__ part) {
+  constexpr int N = ipow3(L);
+  extern __shared__ __align__(16) unsigned char carry_smem[];  // 2 x 3^L elements
+  T (*buf)[N] = reinterpret_cast<T (*)[N]>(carry_smem);
+  const uint64_t t = blockIdx.x;
+  for (int i = threadIdx.x; i < N; i += 256) buf[0][i] = z[t * N + i];
+  __syncthreads();
+  int cur = 0;
+  uint32_t V = 1, nr = N;
+#pragma unroll 1
+  for (int c = 0; c < L; ++c) {
+    const uint32_t V2 = 2 * V + 1, nr2 = nr / 3;
+    for (uint32_t o = threadIdx.x; o < nr2 * V2; o += 256) {
+      const uint32_t r = o / V2, v = o - r * V2;
+      buf[cur ^ 1][o] = carry_gather<T, uint32_t>(buf[cur], V, r, v, c);
+    }
+    __syncthreads();
+    cur ^= 1;
+    V = V2;
+    nr = nr2;
+  }
+  for (uint32_t v = threadIdx.x; v < V; v += 256) part[t * V + v] = buf[cur][v];
+}
+
+// one further axis c: A [nr][2^(c+1) - 1] -> B [nr / 3][2^(c+2) - 1], one thread per output
+// I = uint32_t whenever nr2 * V2 < 2^32 (every case up to D = 22)
+template <class T, class I>
+__global__ void __launch_bounds__(256) carry_step_kernel(const T* __restrict__ A, T* __restrict__ B, uint64_t nr2,
+                                                         int c) {
+  const I V = ((I)2 << c) - 1, V2 = 2 * V + 1;
+  const I total = (I)nr2 * V2;
+  for (I o = (I)blockIdx.x * 256 + threadIdx.x; o < total; o += (I)gridDim.x * 256) {
+    const I r = o / V2, v = o - r * V2;
+    B[o] = carry_gather<T, I>(A, V, r, v, c);
+  }
+}
+
+// f2 -----------------------------------------------------------------------------------
+// max of a nonnegative double array (bit patterns order like the values): atomicMax on u64
+__global__ void __launch_bounds__(256) max_nonneg_kernel(const double* __restrict__ a, uint64_t n,
+                                                         unsigned long long* out) {
+  double m = 0.0;
+  for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256)
+    m = fmax(m, a[i]);
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, s));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// xp[i] = (x[i] / max x)^p  (0 where the maximum is 0); p = 2^sq: sq squarings
+__global__ void __launch_bounds__(256) pnorm_pre_kernel(const double* __restrict__ x, double* __restrict__ xp,
+                                                        uint64_t n, double p, int sq, const unsigned long long* mx) {
+  const double s = __longlong_as_double((long long)*mx);
+  for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256) {
+    double v = s > 0.0 ? x[i] / s : 0.0;
+    if (sq >= 0) {
+      for (int k = 0; k < sq; ++k) v *= v;
+    } else {
+      v = pow(v, p);
+    }
+    xp[i] = v;
+  }
+}
+
+// z[k] = max x * max y * z[k]^(1/p), optionally rounded to the nearest integer; p = 2^sq:
+// sq square roots
+__global__ void __launch_bounds__(256) pnorm_post_kernel(double* __restrict__ z, uint64_t n, double p, int sq,
+                                                         const unsigned long long* mx, int round_to_int) {
+  const double s = __longlong_as_double((long long)mx[0]) * __longlong_as_double((long long)mx[1]);
+  const double ip = 1.0 / p;
+  for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256) {
+    double v = z[i];
+    if (v > 0.0) {
+      if (sq >= 0) {
+        for (int k = 0; k < sq; ++k) v = sqrt(v);
+      } else {
+        v = pow(v, ip);
+      }
+      v *= s;
+    } else {
+      v = 0.0;
+    }
+    z[i] = round_to_int ? rint(v) : v;
+  }
+}
+
+}  // namespace hc

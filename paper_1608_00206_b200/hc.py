@@ -44,6 +44,11 @@ _lib.hc_ep_create.argtypes = [ctypes.POINTER(_P), _I, _I, _I, _I, _I]
 _lib.hc_ep_destroy.argtypes = [_P]
 _lib.hc_ep_local.argtypes = [_P, _P, _P, _P, _P]
 _lib.hc_ep_finish.argtypes = [_P, _P, _P, _P]
+_lib.hc_convolve_difference.argtypes = [_P, _P, _P, _P, _P]
+_lib.hc_carries_work_len.argtypes = [_I]
+_lib.hc_carries_work_len.restype = _U64
+_lib.hc_apply_carries.argtypes = [_I, _I, _P, _P, _P, _P]
+_lib.hc_maxconv_pnorm.argtypes = [_P, _P, _P, _P, ctypes.c_double, _I, _P]
 _lib.hc_launch_count.restype = _U64
 _lib.hc_prof_enable.argtypes = [_I]
 _lib.hc_prof_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_U64)]
@@ -151,6 +156,22 @@ class Plan:
             "hc_convolve_sharded")
         return z_shard
 
+    def convolve_difference(self, x, y, z, stream=None):
+        """hc_convolve_difference: z[k] = P(X - Y = k - 1) digit-wise."""
+        n, m = in_len(self.D), out_len(self.D)
+        _ok(_lib.hc_convolve_difference(self._h, _dev(x, n, self.dtype_code, "x"), _dev(y, n, self.dtype_code, "y"),
+                                        _dev(z, m, self.dtype_code, "z"), _P(_stream_ptr(stream))),
+            "hc_convolve_difference")
+        return z
+
+    def maxconv_pnorm(self, x, y, z, p: float, round_to_int: bool = False, stream=None):
+        """hc_maxconv_pnorm: p-norm estimate of max_{i+j=k} x[i] y[j]."""
+        n, m = in_len(self.D), out_len(self.D)
+        _ok(_lib.hc_maxconv_pnorm(self._h, _dev(x, n, self.dtype_code, "x"), _dev(y, n, self.dtype_code, "y"),
+                                  _dev(z, m, self.dtype_code, "z"), float(p), 1 if round_to_int else 0,
+                                  _P(_stream_ptr(stream))), "hc_maxconv_pnorm")
+        return z
+
     def convolve_host(self, x_host, y_host, z_host, stream=None):
         """Host (CPU, ideally pinned) tensors; copies in, computes, copies this rank's share out."""
         n = in_len(self.D)
@@ -187,6 +208,37 @@ def convolve(x, y, z=None, stream=None):
         z = torch.empty(3 ** D, dtype=x.dtype, device=x.device)
     Plan(D, x.dtype).convolve(x, y, z, stream)
     return z
+
+
+def carries_work_len(D: int) -> int:
+    return int(_lib.hc_carries_work_len(D))
+
+
+def apply_carries(D: int, z, out, work=None, stream=None):
+    """hc_apply_carries: out[m] = sum_{k: sum_b k_b 2^b = m} z[k]."""
+    import torch
+    code = _dtype_code(z.dtype)
+    wl = carries_work_len(D)
+    if wl and work is None:
+        work = torch.empty(wl, dtype=z.dtype, device=z.device)
+    wp = _dev(work, wl, code, "work") if wl else _P(0)
+    _ok(_lib.hc_apply_carries(D, code, _dev(z, out_len(D), code, "z"), _dev(out, (2 << D) - 1, code, "out"), wp,
+                              _P(_stream_ptr(stream))), "hc_apply_carries")
+    return out
+
+
+def conv1d(x, y, out=None, plan=None, stream=None):
+    """Ordinary 1-D convolution of two length-2^D CUDA vectors through the carry-free
+    (hypercube) convolution and the carries (PAPER.md 354-373)."""
+    import torch
+    n = x.numel()
+    D = n.bit_length() - 1
+    plan = plan or Plan(D, x.dtype)
+    z = torch.empty(3 ** D, dtype=x.dtype, device=x.device)
+    plan.convolve(x, y, z, stream)
+    if out is None:
+        out = torch.empty((2 << D) - 1, dtype=x.dtype, device=x.device)
+    return apply_carries(D, z, out, stream=stream)
 
 
 def ep_range(D: int, k: int, ngpu: int, rank: int):

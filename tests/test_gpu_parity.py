@@ -303,3 +303,100 @@ def test_output_at_odd_element_offset(hc, orc):
         torch.cuda.synchronize()
         assert int(buf[0]) == 0
         assert np.array_equal(buf[1:].cpu().numpy(), orc.conv(x, y))
+
+
+# ---- applications ---------------------------------------------------------
+@pytest.fixture(scope="module")
+def apps(orc):
+    import oracle.apps as a
+    return a
+
+
+@pytest.mark.parametrize("D,dtype", [(1, "int64"), (3, "int64"), (7, "float64"), (9, "int64"), (12, "float64"),
+                                     (13, "int64")])
+def test_difference_pmf(hc, apps, D, dtype):
+    # f4: P(X - Y = k - 1) against its definition (every pair, digit-wise difference)
+    if dtype == "int64":
+        x, y = hcgen.make_pair(D, "int64", "uniform", 9100 + D, -100, 100)
+    else:
+        x, y = hcgen.make_pair(D, "float64", "exp_norm", 9100 + D)
+    tdt = torch.int64 if dtype == "int64" else torch.float64
+    z = torch.empty(3 ** D, dtype=tdt, device="cuda")
+    hc.Plan(D, dtype).convolve_difference(_gpu(x), _gpu(y), z)
+    torch.cuda.synchronize()
+    _assert_close(z.cpu().numpy(), apps.difference_pmf(x, y), x, y)
+
+
+@pytest.mark.parametrize("D", [1, 4, 8, 9, 11, 14])
+def test_conv1d_via_carries_int64(hc, D):
+    # f1: carry-free convolution + carries = the ordinary 1-D convolution (numpy's definition)
+    x = hcgen.uniform_int(9200 + D, 0, 1 << D, -10 ** 6, 10 ** 6)
+    y = hcgen.uniform_int(9200 + D, 1, 1 << D, -10 ** 6, 10 ** 6)
+    out = hc.conv1d(_gpu(x), _gpu(y))
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), np.convolve(x, y))
+
+
+def test_carries_fp64_and_d20_sampled(hc, apps, orc):
+    # fp64: the carries of the GPU hypercube output equal the oracle's carries of the oracle's
+    # convolution; D = 20 int64: sampled m against sum_i x[i] y[m - i]
+    D = 10
+    x, y = hcgen.make_pair(D, "float64", "exp_norm", 9300)
+    out = hc.conv1d(_gpu(x), _gpu(y)).cpu().numpy()
+    want = apps.conv1d_carryfree_then_carries(x, y)
+    assert np.max(np.abs(out - want)) <= 1e-12 * float(x.sum() * y.sum())
+    D = 20
+    x = hcgen.uniform_int(9301, 0, 1 << D, 0, 1 << 16)
+    y = hcgen.uniform_int(9301, 1, 1 << D, 0, 1 << 16)
+    out = hc.conv1d(_gpu(x), _gpu(y)).cpu().numpy()
+    rng = np.random.default_rng(20)
+    for m in list(rng.integers(0, (2 << D) - 1, 200)) + [0, 1, (1 << D) - 1, (2 << D) - 2]:
+        lo, hi = max(0, m - (1 << D) + 1), min(m, (1 << D) - 1)
+        i = np.arange(lo, hi + 1)
+        assert out[m] == int((x[i].astype(object) * y[m - i].astype(object)).sum())
+
+
+def _power_domain(E, mx, my, p):
+    return np.where(E > 0, (E / (mx * my)) ** p, 0.0)
+
+
+@pytest.mark.parametrize("D,p", [(6, 2.0), (8, 16.0), (10, 64.0), (13, 8.0)])
+def test_maxconv_pnorm_estimate(hc, apps, D, p):
+    # f2: the GPU p-norm estimate against the oracle's (same formula on Algorithm 1).  The sum
+    # of p-th powers goes through the hot path, whose tolerance is absolute (1e-12 x the scaled
+    # masses, R4): compare there on every cell, and compare the estimates relatively
+    # on the cells whose power sum stands above that noise (R11).
+    x = hcgen.uniform_int(9400 + D, 0, 1 << D, 0, 1000).astype(np.float64)
+    y = hcgen.uniform_int(9400 + D, 1, 1 << D, 0, 1000).astype(np.float64)
+    z = torch.empty(3 ** D, dtype=torch.float64, device="cuda")
+    hc.Plan(D, "float64").maxconv_pnorm(_gpu(x), _gpu(y), z, p)
+    torch.cuda.synchronize()
+    got, want = z.cpu().numpy(), apps.maxconv_pnorm(x, y, p)
+    mx, my = x.max(), y.max()
+    mass = float(((x / mx) ** p).sum() * ((y / my) ** p).sum())
+    sg, sw = _power_domain(got, mx, my, p), _power_domain(want, mx, my, p)
+    assert np.max(np.abs(sg - sw)) <= 1e-12 * mass
+    good = sw >= 1e-6 * mass
+    assert good.sum() > 0
+    assert np.allclose(got[good], want[good], rtol=1e-10, atol=0)
+    M = apps.maxconv_exact(x, y)
+    assert (got[good] >= M[good] * (1 - 1e-10)).all() and (got[good] <= M[good] * 2.0 ** (D / p) * (1 + 1e-10)).all()
+
+
+def test_maxconv_pnorm_exact_rounding(hc, apps):
+    # PAPER.md 346-352: bounded integers and p with M (n^(1/p) - 1) < 0.5 -> rounding gives the
+    # exact max-convolution, on every cell whose power sum the fp64 pipeline resolves
+    # (R11), which includes the global maximum
+    D = 8
+    x = hcgen.uniform_int(9500, 0, 1 << D, 0, 3).astype(np.float64)
+    y = hcgen.uniform_int(9500, 1, 1 << D, 0, 3).astype(np.float64)
+    p = float(np.ceil(np.log(2.0 ** D) / np.log(1 + 0.5 / 9.0))) + 1
+    z = torch.empty(3 ** D, dtype=torch.float64, device="cuda")
+    hc.Plan(D, "float64").maxconv_pnorm(_gpu(x), _gpu(y), z, p, round_to_int=True)
+    torch.cuda.synchronize()
+    got, M = z.cpu().numpy(), apps.maxconv_exact(x, y)
+    mx, my = x.max(), y.max()
+    mass = float(((x / mx) ** p).sum() * ((y / my) ** p).sum())
+    resolved = (M / (mx * my)) ** p >= 1e-6 * mass
+    assert resolved[np.argmax(M)] and resolved.sum() > 0
+    assert np.array_equal(got[resolved], M[resolved])
