@@ -164,7 +164,7 @@ cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const Sla
   static int grid_max = 0;
   cudaError_t e = t8_grid(kern, grid_max);
   if (e != cudaSuccess) return e;
-  const uint64_t items = (uint64_t)a.nslab * (upow3(M) + upow3(8) / P2W);
+  const uint64_t items = (uint64_t)a.nslab * (upow3(M) + upow3(8) / (P2W * T8_P2CH));
   const unsigned grid = (unsigned)(items < (uint64_t)grid_max ? items : (uint64_t)grid_max);
   e = cudaMemsetAsync(a.ctr, 0, sizeof(uint32_t) * (1 + (size_t)a.nslab), st);
   if (e != cudaSuccess) return e;

@@ -444,6 +444,10 @@ __device__ __forceinline__ ItemDec decode_item(uint32_t q, uint32_t ns, uint32_t
 #endif
 constexpr int T8_QN = HC_QN;  // claimed items held per CTA
 constexpr uint32_t T8_EXH = 0xffffffffu;
+#ifndef HC_P2CH
+#define HC_P2CH 3
+#endif
+constexpr int T8_P2CH = HC_P2CH;  // 9-column chunks per pass-2 item
 
 struct Slot {
   uint32_t q;            // claim index, T8_EXH = past the end
@@ -455,7 +459,7 @@ template <class T, int M>
 __global__ void __launch_bounds__(T8_NT, 2)
 slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__ z, SlabArgs args) {
   constexpr uint32_t N1 = (uint32_t)ipow3(M);
-  constexpr uint32_t N2 = (uint32_t)(ipow3(8) / P2W);
+  constexpr uint32_t N2 = (uint32_t)(ipow3(8) / (P2W * T8_P2CH));
   constexpr uint64_t SLAB = upow3(M + 8);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -602,8 +606,13 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       // barrier): the reads below are ordered after it by that control dependency and the
       // barrier, and go to L2 (.cg), where the producers' fenced stores already are
       if (threadIdx.x == T8_SCHED) pump();
-      p2_item<T, M, 8>(zs, it.r, sm, threadIdx.x < 243 ? (int)threadIdx.x : -1, T8_SCHED, signal,
-                       [] { __syncthreads(); });
+      // three 9-column chunks per item (a third as many items to schedule)
+#pragma unroll 1
+      for (int ch = 0; ch < T8_P2CH; ++ch) {
+        if (ch) __syncthreads();  // the exchange buffer is rewritten by the next chunk
+        p2_item<T, M, 8>(zs, it.r * T8_P2CH + ch, sm, threadIdx.x < 243 ? (int)threadIdx.x : -1,
+                         ch == 0 ? T8_SCHED : -1, signal, [] { __syncthreads(); });
+      }
       PH_MARK(4);
     }
     __syncthreads();  // the item's smem is free
