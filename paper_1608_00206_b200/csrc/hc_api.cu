@@ -148,6 +148,28 @@ cudaError_t t8_grid(K kern, int& grid_max) {
 template <class T>
 cudaError_t launch_tile8(const T* x, const T* y, T* z, int D, uint64_t slab0, uint64_t nslab, uint64_t nitems,
                          cudaStream_t st) {
+  // HC_TILE_WS=1: warp-specialised variant (tilews_kernel); measured slower than the fork-join
+  // tile8_kernel on B200 (batched D=8: 1.44 vs 1.17 ms), kept for experiments
+  static const int ws = getenv("HC_TILE_WS") ? atoi(getenv("HC_TILE_WS")) : 0;
+  if (ws) {
+    auto kern = tilews_kernel<T>;
+    static int grid_max = 0;
+    if (!grid_max) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TWSCfg::SMEM);
+      if (e != cudaSuccess) return e;
+      int occ = 0, dev = 0, sms = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WS_NT, TWSCfg::SMEM);
+      if (e != cudaSuccess) return e;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (occ < 1) return cudaErrorInvalidConfiguration;
+      grid_max = occ * sms;
+    }
+    const unsigned grid = (unsigned)(nitems < (uint64_t)grid_max ? nitems : (uint64_t)grid_max);
+    LaunchScope ls("tile", st);
+    kern<<<grid, WS_NT, TWSCfg::SMEM, st>>>(x, y, z, D, slab0, nslab, nitems);
+    return cudaGetLastError();
+  }
   auto kern = tile8_kernel<T>;
   static int grid_max = 0;
   cudaError_t e = t8_grid(kern, grid_max);

@@ -327,4 +327,144 @@ slabws_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict_
   }
 }
 
+// ---- warp-specialised single-level engine (8 <= D <= 12, batched D >= 8) ---------------
+// Compute group: tiles w = blockIdx.x, + gridDim.x, ... (item w: batch w / nslab, top index
+// slab0 + w % nslab; prefetcher over the same sequence), pair loop + register-axes inverse,
+// tile to S.  Epilogue group: B and A axes, final streaming store to z[w * 6561 ...].  The
+// last hand-off carries an end marker.
+struct TWSCfg {
+  static constexpr int S_OFF = 2 * PS_SZ + T8_NRAW * RS_SZ;
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(S_OFF + 6568);
+};
+
+template <class T>
+__global__ void __launch_bounds__(WS_NT, 1)
+tilews_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z, int D, uint64_t slab0,
+              uint64_t nslab, uint64_t nitems) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  T* P = sm;
+  T* R = sm + 2 * PS_SZ;
+  T* S = sm + TWSCfg::S_OFF;
+  __shared__ __align__(8) uint64_t raw_bar[T8_NRAW];
+  __shared__ __align__(8) uint64_t full_bar, empty_bar;
+  __shared__ Prefetch pf;
+  __shared__ unsigned long long s_dst;  // element offset of the tile in S, ~0ull = end
+  const int tid = threadIdx.x;
+  constexpr unsigned long long END = ~0ull;
+  if (tid == 0) {
+    for (int i = 0; i < T8_NRAW; ++i) mbar_init(&raw_bar[i], 1);
+    mbar_init(&full_bar, 1);
+    mbar_init(&empty_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid < 256) {
+    // ------------------------------- compute group --------------------------------
+    RawRing rr{raw_bar, 0, 0};
+    const int k = D - 8;
+    const uint64_t pol_in = policy_evict_last();
+    if (tid == WS_CLEAD) {
+      pf.left = 0;
+      pf.pos = 0xffffffffu;
+    }
+    auto next = [&](Prefetch& c) -> bool {
+      const uint32_t np = c.pos + 1;
+      const uint64_t w = blockIdx.x + (uint64_t)np * gridDim.x;
+      if (w >= nitems) return false;
+      const uint64_t b = w / nslab;
+      uint32_t base, freeb;
+      trit_split(slab0 + (w - b * nslab), k, base, freeb);
+      c.pos = np;
+      c.sx0 = x + (b << D);
+      c.sy0 = y + (b << D);
+      c.stride = 256;
+      c.base = base;
+      c.freeb = freeb;
+      c.s = 0;
+      c.left = 1 << __popc(freeb);
+      return true;
+    };
+    auto pump = [&]() { pf_pump<T>(pf, rr, R, pol_in, next); };
+    const int w8 = tid >> 5, lane = tid & 31;
+    const bool unit = tid < 243;
+    const int u = t8_unit(tid);
+    const int ea2 = u / 81, eS = u - 81 * ea2;
+    const int f1es = t8_f1_es(w8);
+    auto f1 = [&](T* Pd) {
+      if (f1es >= 0) t8_f1<T>(R + t8_wait(rr) * RS_SZ, Pd, f1es, lane);
+      else ++rr.done;
+    };
+    uint32_t ntile = 0;
+    for (uint64_t w = blockIdx.x; w < nitems; w += gridDim.x) {
+      const uint64_t b = w / nslab;
+      uint32_t base, freeb;
+      trit_split(slab0 + (w - b * nslab), k, base, freeb);
+      const int npairs = 1 << __popc(freeb);
+      if (tid == WS_CLEAD) pump();
+      f1(P);
+      bar_named(WS_BAR_C, 256);
+      T acc[27];
+#pragma unroll
+      for (int i = 0; i < 27; ++i) acc[i] = T(0);
+      for (int p = 0; p < npairs; ++p) {
+        if (tid == WS_CLEAD) pump();
+        if (p + 1 < npairs) f1(P + ((p + 1) & 1) * PS_SZ);
+        if (unit) t8_f2<T>(P + (p & 1) * PS_SZ, ea2, eS, acc);
+        bar_named(WS_BAR_C, 256);
+      }
+      if (tid == WS_CLEAD) pump();
+      if (unit) inv_reg<3, T>(acc);
+      if (ntile > 0) mbar_wait(&empty_bar, (ntile - 1) & 1);
+      if (unit) {
+#pragma unroll
+        for (int i = 0; i < 27; ++i) S[u * 27 + i] = acc[i];
+      }
+      if (tid == WS_CLEAD) s_dst = (unsigned long long)w * 6561ull;
+      bar_named(WS_BAR_C, 256);
+      if (tid == WS_CLEAD) mbar_arrive1(&full_bar);
+      ++ntile;
+    }
+    if (tid == WS_CLEAD) {  // end marker, once the epilogue has taken the last tile
+      if (ntile > 0) mbar_wait(&empty_bar, (ntile - 1) & 1);
+      s_dst = END;
+      mbar_arrive1(&full_bar);
+    }
+  } else {
+    // ------------------------------- epilogue group -------------------------------
+    const int et = tid - 256;
+    const bool etask = et < 243;
+    for (uint32_t nt = 0;; ++nt) {
+      mbar_wait(&full_bar, nt & 1);
+      const unsigned long long dst = s_dst;
+      if (dst == END) break;
+      if (etask) {  // B axes
+        const int a = et / 27, cc = et - 27 * a;
+        T v[27];
+#pragma unroll
+        for (int e = 0; e < 27; ++e) v[e] = S[a * 729 + e * 27 + cc];
+        inv_reg<3, T>(v);
+#pragma unroll
+        for (int e = 0; e < 27; ++e) S[a * 729 + e * 27 + cc] = v[e];
+      }
+      bar_named(WS_BAR_E, 256);
+      if (etask) {  // A axes + final store
+        T* zt = z + dst;
+#pragma unroll 1
+        for (int r = 0; r < 3; ++r) {
+          const int col = r * 243 + et;
+          T v[9];
+#pragma unroll
+          for (int e = 0; e < 9; ++e) v[e] = S[e * 729 + col];
+          inv_reg<2, T>(v);
+#pragma unroll
+          for (int e = 0; e < 9; ++e) st_cs(zt + e * 729 + col, v[e]);
+        }
+      }
+      bar_named(WS_BAR_E, 256);  // S fully read
+      if (tid == WS_ELEAD) mbar_arrive1(&empty_bar);
+    }
+  }
+}
+
 }  // namespace hc
