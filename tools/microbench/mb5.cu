@@ -22,6 +22,34 @@ __global__ void __launch_bounds__(T8_NT, 2) k_pairs(int iters, double* sink) {
   double acc[27];
 #pragma unroll
   for (int i = 0; i < 27; ++i) acc[i] = 0;
+  if (MODE == 5) {  // full / empty mbarriers per P buffer instead of one CTA barrier per pair
+    __shared__ __align__(8) uint64_t fullb[2], emptyb[2];
+    if (tid == 0) {
+      mbar_init(&fullb[0], 3); mbar_init(&fullb[1], 3);
+      mbar_init(&emptyb[0], 8); mbar_init(&emptyb[1], 8);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int es = t8_f1_es(w);
+    if (es >= 0) {  // F1 of pair 0
+      t8_f1<double>(R, P, es, lane);
+      __syncwarp();
+      if (lane == 0) { asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(&fullb[0])) : "memory"); }
+    }
+    for (int p = 0; p < iters; ++p) {
+      const int b1 = (p + 1) & 1;
+      if (es >= 0 && p + 1 < iters) {
+        if (p + 1 >= 2) mbar_wait(&emptyb[b1], ((p - 1) / 2) & 1);
+        t8_f1<double>(R + ((p + 1) % T8_NRAW) * RS_SZ, P + b1 * PS_SZ, es, lane);
+        __syncwarp();
+        if (lane == 0) { asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(&fullb[b1])) : "memory"); }
+      }
+      mbar_wait(&fullb[p & 1], (p / 2) & 1);
+      if (unit) t8_f2<double>(P + (p & 1) * PS_SZ, ea2, eS, acc);
+      __syncwarp();
+      if (lane == 0) { asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(&emptyb[p & 1])) : "memory"); }
+    }
+  } else
   for (int p = 0; p < iters; ++p) {
     if (MODE != 1 && t8_f1_es(w) >= 0) t8_f1<double>(R + (p % T8_NRAW) * RS_SZ, P + ((p + 1) & 1) * PS_SZ, t8_f1_es(w), lane);
     if (MODE == 4 && unit) {  // F2 arithmetic only: inputs from registers (no shared loads)
@@ -65,12 +93,13 @@ int main() {
   double* sink;
   cudaMalloc(&sink, 8);
   const int iters = 20000;
-  const char* names[] = {"F1+F2+bar", "F2+bar", "F1+bar", "F1+F2 nobar", "F2 math only"};
+  const char* names[] = {"F1+F2+bar", "F2+bar", "F1+bar", "F1+F2 nobar", "F2 math only", "F1+F2 mbarriers"};
   for (int ctas = 1; ctas <= 2; ++ctas) {
     const int grid = sms * ctas;
-    for (int m = 0; m < 5; ++m) {
+    for (int m = 0; m < 6; ++m) {
       float ms = m == 0 ? run<0>(grid, iters, sink) : m == 1 ? run<1>(grid, iters, sink)
-               : m == 2 ? run<2>(grid, iters, sink) : m == 3 ? run<3>(grid, iters, sink) : run<4>(grid, iters, sink);
+               : m == 2 ? run<2>(grid, iters, sink) : m == 3 ? run<3>(grid, iters, sink)
+               : m == 4 ? run<4>(grid, iters, sink) : run<5>(grid, iters, sink);
       // clk per pair iteration per SM (all CTAs on the SM together)
       const double clk_per = (ms * 1e-3) * (clk * 1e3) / ((double)iters * ctas);
       printf("ctas/SM %d %-12s %.3f ms  %.0f clk per pair-iteration per SM\n", ctas, names[m], ms, clk_per);
