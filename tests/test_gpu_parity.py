@@ -400,3 +400,56 @@ def test_maxconv_pnorm_exact_rounding(hc, apps):
     resolved = (M / (mx * my)) ** p >= 1e-6 * mass
     assert resolved[np.argmax(M)] and resolved.sum() > 0
     assert np.array_equal(got[resolved], M[resolved])
+
+
+def test_scheduler_race_stress(hc, orc):
+    # the persistent kernels hand work out through atomics, mbarriers and completion
+    # counters: repeated runs (whole outputs and uneven shards) must all be bit-identical to
+    # Algorithm 1 -- a race in the schedule would show up as run-to-run differences
+    for D, seed in ((13, 1), (15, 2), (16, 3)):
+        x, y = hcgen.make_pair(D, "int64", "uniform", 6000 + seed, -(1 << 20), 1 << 20)
+        want = orc.conv(x, y)
+        xs, ys = _gpu(x), _gpu(y)
+        p = hc.Plan(D, "int64")
+        z = torch.empty(3 ** D, dtype=torch.int64, device="cuda")
+        for _ in range(6):
+            z.fill_(-1)
+            p.convolve(xs, ys, z)
+            torch.cuda.synchronize()
+            assert np.array_equal(z.cpu().numpy(), want)
+        for n in {13: (), 15: (2, 3), 16: (2, 5)}[D]:  # shards need 3^k >= n slabs
+            parts = []
+            for r in range(n):
+                pr = hc.Plan(D, "int64", n, r)
+                b, e = pr.shard_info()
+                zs = torch.empty(e - b, dtype=torch.int64, device="cuda")
+                pr.convolve_sharded(xs, ys, zs)
+                parts.append(zs)
+            torch.cuda.synchronize()
+            assert np.array_equal(torch.cat(parts).cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("var", ["HC_SLAB_WS", "HC_TILE_WS"])
+def test_warp_specialised_variants(var):
+    # the opt-in warp-specialised kernels (hc_ws.cuh) are selected by environment variables
+    # read once per process: run them in a child process against the oracle
+    import subprocess
+    import sys
+    import os
+    code = (
+        "import sys; sys.path.insert(0, '.'); import numpy as np, torch, hcgen, oracle;"
+        "import paper_1608_00206_b200.hc as hc; oracle.build()\n"
+        "for D in (9, 11, 13, 15, 16):\n"
+        "    x, y = hcgen.make_pair(D, 'int64', 'uniform', 7100 + D, -999, 999)\n"
+        "    z = torch.empty(3 ** D, dtype=torch.int64, device='cuda')\n"
+        "    hc.Plan(D, 'int64').convolve(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), z)\n"
+        "    torch.cuda.synchronize(); assert np.array_equal(z.cpu().numpy(), oracle.conv(x, y)), D\n"
+        "xb, yb = hcgen.make_batched_fast(5, 8, 0, 255, 71)\n"
+        "zb = torch.empty((5, 6561), dtype=torch.int64, device='cuda')\n"
+        "hc.convolve_batched(torch.from_numpy(xb).cuda(), torch.from_numpy(yb).cuda(), zb)\n"
+        "torch.cuda.synchronize(); assert np.array_equal(zb.cpu().numpy(), oracle.conv_batched(xb, yb))\n"
+        "print('ok')\n")
+    env = dict(os.environ, **{var: "1", "HC_SLAB_LAG": "2"})
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
