@@ -46,7 +46,7 @@ __device__ __forceinline__ T carry_gather(const T* A, I V, I r, I v, int c) {
 template <class T, int L>
 __global__ void __launch_bounds__(256) carry_tile_kernel(const T* __restrict__ z, T* __restrict__ part) {
   constexpr int N = ipow3(L);
-  extern __shared__ __align__(16) unsigned char carry_smem[];  // 2 x 3^L elements
+  extern __shared__ __align__(128) unsigned char carry_smem[];  // 2 x 3^L elements
   T (*buf)[N] = reinterpret_cast<T (*)[N]>(carry_smem);
   const uint64_t t = blockIdx.x;
   for (int i = threadIdx.x; i < N; i += 256) buf[0][i] = z[t * N + i];

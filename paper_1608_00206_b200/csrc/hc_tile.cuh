@@ -126,7 +126,7 @@ __device__ __forceinline__ void p1_tile(const T* __restrict__ x, const T* __rest
                                         int k, int M, uint64_t tT, uint32_t eU, T* sm) {
   using Cfg = TileCfg<T, C, B, A>;
   constexpr int NT = Cfg::NT, L = Cfg::L, NP = Cfg::NP;
-  constexpr int P3B = ipow3(B), P3C = ipow3(C), P2A = 1 << A, P2C = 1 << C;
+  constexpr int P3B = ipow3(B), P3C = ipow3(C), P2C = 1 << C;
   static_assert(B > 0, "p1_tile needs B > 0");
   T* S = sm;                  // [3^A][3^B][3^C] after the pair loop (aliases the stages)
   const int tid = threadIdx.x;
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(TileCfg<T, C, B, A>::NT)
 tile_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z, int D,
             uint64_t slab0, uint64_t nslab) {
   using Cfg = TileCfg<T, C, B, A>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   const uint64_t w = blockIdx.x;
   const uint64_t b = w / nslab;
