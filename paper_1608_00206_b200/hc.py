@@ -298,6 +298,13 @@ def ep_exchange(w, wt, D: int, k: int, rank: int, world: int, dist=None):
     if world == 1 or dist is None:
         wt.view(e1 - e0, c1 - c0).copy_(w.view(e1 - e0, -1)[:, c0:c1])
         return wt
+    if w.is_cuda and dist.get_backend() == "gloo":
+        # gloo's point-to-point is CPU-only: stage through host memory (testing several ranks
+        # on one device); NCCL exchanges the device buffers directly
+        wt_h = wt.cpu()
+        ep_exchange(w.cpu(), wt_h, D, k, rank, world, dist)
+        wt.copy_(wt_h)
+        return wt
     wv = w.view(e1 - e0, -1)
     wtv = wt.view(3 ** k, c1 - c0)
     ops = []

@@ -45,3 +45,24 @@ def test_bench_two_ranks_share_one_gpu():
     assert r.returncode == 0, r.stderr[-3000:]
     d = _json_line(r.stdout)
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "output-split x2"
+
+
+@pytest.mark.parametrize("args,parallelism", [
+    (["--workload", "c3_d16_i64", "--variant", "evalpoint", "--ep-k", "2"], "evalpoint k=2 x2 (all-to-all)"),
+    (["--workload", "c5_d22_f64", "--steps", "1", "--no-cpu-baseline"],
+     "8 output-split shards streamed through one buffer, 4 per rank x2"),
+])
+def test_bench_two_ranks_variants(args, parallelism):
+    # the evaluation-point variant (exchange staged through host memory under gloo) and the
+    # streamed D = 22 workload, two ranks on the one GPU
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
+           "--steps", "2", "--warmup", "3", "--no-e2e", "--dist-backend", "gloo"] + args
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _json_line(r.stdout)
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == parallelism
