@@ -763,6 +763,21 @@ cudaError_t carry_tile(const T* z, T* part, uint64_t ntiles, cudaStream_t st) {
   k<<<(unsigned)ntiles, 256, sm, st>>>(z, part);
   return cudaGetLastError();
 }
+// one global combining step for axis c (compile-time c, 32-bit indices when they fit)
+template <class T, int C>
+cudaError_t carry_step_c(const T* A, T* B, uint64_t nr2, uint64_t n2, cudaStream_t st) {
+  if (n2 < (1ull << 32)) carry_step_kernel<T, uint32_t, C><<<ew_grid(n2), 256, 0, st>>>(A, B, nr2);
+  else carry_step_kernel<T, uint64_t, C><<<ew_grid(n2), 256, 0, st>>>(A, B, nr2);
+  return cudaGetLastError();
+}
+template <class T, int C = 8>
+cudaError_t carry_step(const T* A, T* B, uint64_t nr2, uint64_t n2, int c, cudaStream_t st) {
+  if constexpr (C < HC_MAX_D) {
+    if (c == C) return carry_step_c<T, C>(A, B, nr2, n2, st);
+    return carry_step<T, C + 1>(A, B, nr2, n2, c, st);
+  }
+  return cudaErrorInvalidValue;
+}
 template <class T>
 cudaError_t apply_carries_t(int D, const T* z, T* out, T* work, cudaStream_t st) {
   const int L = D < 8 ? D : 8;
@@ -789,9 +804,7 @@ cudaError_t apply_carries_t(int D, const T* z, T* out, T* work, cudaStream_t st)
     T* B = (c + 1 == D) ? out : (A == work ? work + half : work);
     const uint64_t n2 = nr2 * ((4ull << c) - 1);
     LaunchScope ls("carry", st);
-    if (n2 < (1ull << 32)) carry_step_kernel<T, uint32_t><<<ew_grid(n2), 256, 0, st>>>(A, B, nr2, c);
-    else carry_step_kernel<T, uint64_t><<<ew_grid(n2), 256, 0, st>>>(A, B, nr2, c);
-    e = cudaGetLastError();
+    e = carry_step<T>(A, B, nr2, n2, c, st);
     if (e != cudaSuccess) return e;
     A = B;
     nr = nr2;

@@ -41,43 +41,52 @@ __device__ __forceinline__ T carry_gather(const T* A, I V, I r, I v, int c) {
   return s;
 }
 
+// one combining step inside the tile: axis C of a 3^L tile, compile-time sizes (so the index
+// divisions compile to multiply-shifts)
+template <class T, int L, int C>
+__device__ __forceinline__ void carry_tile_step(const T* A, T* B) {
+  constexpr uint32_t V = (2u << C) - 1, V2 = 2 * V + 1;
+  constexpr uint32_t NR2 = (uint32_t)ipow3(L - C - 1);
+  for (uint32_t o = threadIdx.x; o < NR2 * V2; o += 256) {
+    const uint32_t r = o / V2, v = o - r * V2;
+    B[o] = carry_gather<T, uint32_t>(A, V, r, v, C);
+  }
+}
+template <class T, int L, int C>
+__device__ __forceinline__ void carry_tile_steps(T* b0, T* b1) {
+  if constexpr (C < L) {
+    carry_tile_step<T, L, C>(b0, b1);
+    __syncthreads();
+    carry_tile_steps<T, L, C + 1>(b1, b0);
+  }
+}
+
 // tile of the low L = min(D, 8) axes (3^L values of z) -> 2^(L+1) - 1 partial sums, combining
 // axis 0, 1, ..., L-1 in shared memory; grid = 3^(D-L) tiles, block 256
 template <class T, int L>
 __global__ void __launch_bounds__(256) carry_tile_kernel(const T* __restrict__ z, T* __restrict__ part) {
   constexpr int N = ipow3(L);
   extern __shared__ __align__(128) unsigned char carry_smem[];  // 2 x 3^L elements
-  T (*buf)[N] = reinterpret_cast<T (*)[N]>(carry_smem);
+  T* b0 = reinterpret_cast<T*>(carry_smem);
+  T* b1 = b0 + N;
   const uint64_t t = blockIdx.x;
-  for (int i = threadIdx.x; i < N; i += 256) buf[0][i] = z[t * N + i];
+  for (int i = threadIdx.x; i < N; i += 256) b0[i] = z[t * N + i];
   __syncthreads();
-  int cur = 0;
-  uint32_t V = 1, nr = N;
-#pragma unroll 1
-  for (int c = 0; c < L; ++c) {
-    const uint32_t V2 = 2 * V + 1, nr2 = nr / 3;
-    for (uint32_t o = threadIdx.x; o < nr2 * V2; o += 256) {
-      const uint32_t r = o / V2, v = o - r * V2;
-      buf[cur ^ 1][o] = carry_gather<T, uint32_t>(buf[cur], V, r, v, c);
-    }
-    __syncthreads();
-    cur ^= 1;
-    V = V2;
-    nr = nr2;
-  }
-  for (uint32_t v = threadIdx.x; v < V; v += 256) part[t * V + v] = buf[cur][v];
+  carry_tile_steps<T, L, 0>(b0, b1);
+  // after L steps (ping-pong) the result is in b0 when L is even, b1 when odd
+  const T* res = (L & 1) ? b1 : b0;
+  constexpr uint32_t V = (2u << L) - 1;
+  for (uint32_t v = threadIdx.x; v < V; v += 256) part[t * V + v] = res[v];
 }
 
-// one further axis c: A [nr][2^(c+1) - 1] -> B [nr / 3][2^(c+2) - 1], one thread per output
-// I = uint32_t whenever nr2 * V2 < 2^32 (every case up to D = 22)
-template <class T, class I>
-__global__ void __launch_bounds__(256) carry_step_kernel(const T* __restrict__ A, T* __restrict__ B, uint64_t nr2,
-                                                         int c) {
-  const I V = ((I)2 << c) - 1, V2 = 2 * V + 1;
+// one further axis C in global memory: A [nr][2^(C+1) - 1] -> B [nr / 3][2^(C+2) - 1]
+template <class T, class I, int C>
+__global__ void __launch_bounds__(256) carry_step_kernel(const T* __restrict__ A, T* __restrict__ B, uint64_t nr2) {
+  constexpr I V = ((I)2 << C) - 1, V2 = 2 * V + 1;
   const I total = (I)nr2 * V2;
   for (I o = (I)blockIdx.x * 256 + threadIdx.x; o < total; o += (I)gridDim.x * 256) {
     const I r = o / V2, v = o - r * V2;
-    B[o] = carry_gather<T, I>(A, V, r, v, c);
+    B[o] = carry_gather<T, I>(A, V, r, v, C);
   }
 }
 
