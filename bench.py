@@ -229,10 +229,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of oracle work per reference step")
-    ap.add_argument("--variant", default="split", choices=["split", "evalpoint"],
+    ap.add_argument("--variant", default="split", choices=["split", "evalpoint", "evalpoint-peer"],
                     help="multi-GPU scheme: 'split' = zero-communication output split (default); "
                          "'evalpoint' = top-axis evaluation points per rank + all-to-all + top inverse "
-                         "(BASELINE north_star (4))")
+                         "(BASELINE north_star (4)); 'evalpoint-peer' = the same with the exchange fused "
+                         "into the top inverse as direct peer reads (SURVEY §8(f) f3)")
     ap.add_argument("--ep-k", type=int, default=4, help="top axes of the evalpoint variant")
     ap.add_argument("--vshards", type=int, default=8,
                     help="c5 (D=22, 251 GB of output): the output is computed as this many shards of the "
@@ -310,20 +311,33 @@ def main():
         in_bytes = 2 * 2 ** D * 8
         prof_name = "slab"
         plan = None  # no host-buffer e2e for the application rows
-    elif args.variant == "evalpoint":
+    elif args.variant in ("evalpoint", "evalpoint-peer"):
         ep = hc.EPPlan(D, args.ep_k, str(x_np.dtype), world, rank)
         nc = 3 ** (D - args.ep_k)
         w_ep = torch.empty((ep.e1 - ep.e0) * nc, dtype=tdt, device="cuda")
-        wt = torch.empty(3 ** args.ep_k * (ep.c1 - ep.c0), dtype=tdt, device="cuda")
-        z = torch.empty_like(wt)
+        z = torch.empty(3 ** args.ep_k * (ep.c1 - ep.c0), dtype=tdt, device="cuda")
         n_local = z.numel()
         n_total = 3 ** D
         xdist = dist if world > 1 else None
+        if args.variant == "evalpoint":
+            wt = torch.empty_like(z)
 
-        def step():
-            ep.local(xg, yg, w_ep)
-            hc.ep_exchange(w_ep, wt, D, args.ep_k, rank, world, xdist)
-            ep.finish(wt, z)
+            def step():
+                ep.local(xg, yg, w_ep)
+                hc.ep_exchange(w_ep, wt, D, args.ep_k, rank, world, xdist)
+                ep.finish(wt, z)
+        else:
+            w_all = hc.ep_peer_buffers(w_ep, rank, world, xdist)
+
+            def step():
+                ep.local(xg, yg, w_ep)
+                if xdist is not None:  # every rank's w is complete before anyone reads it
+                    torch.cuda.synchronize()
+                    xdist.barrier()
+                ep.finish_peer(w_all, z)
+                if xdist is not None:  # ... and read before the next step overwrites it
+                    torch.cuda.synchronize()
+                    xdist.barrier()
         in_bytes = 2 * 2 ** D * 8
         prof_name = "slab"
         plan = None
@@ -440,6 +454,7 @@ def main():
             "config": {"workload": wl, "desc": w["desc"], "D": D, "output_entries": n_total,
                        "variant": w.get("app", args.variant),
                        "parallelism": (f"evalpoint k={args.ep_k} x{world} (all-to-all)" if args.variant == "evalpoint"
+                                       else f"evalpoint k={args.ep_k} x{world} (peer reads)" if args.variant == "evalpoint-peer"
                                        else (f"{args.vshards} output-split shards streamed through one buffer, "
                                              f"{args.vshards // world} per rank x{world}" if wl == "c5_d22_f64"
                                              else (f"output-split x{world}" if world > 1 else "single"))),

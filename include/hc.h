@@ -132,6 +132,13 @@ hc_status hc_ep_local(hc_ep_t p, const void* x, const void* y, void* w, void* st
  * ncols = col_end - col_begin; z must not alias wt. */
 hc_status hc_ep_finish(hc_ep_t p, const void* wt, void* z, void* stream);
 
+/* f3: the exchange fused into the final step.  w_ranks[r] is rank r's
+ * hc_ep_local output (device pointers; on a multi-GPU node peer-mapped buffers of the other
+ * ranks, e.g. CUDA IPC / symmetric memory, read over NVLink), ngpu entries; z = [3^k][ncols]
+ * as in hc_ep_finish.  No gathered copy of w is made: each thread reads its column's 3^k
+ * values straight from their owners' buffers. */
+hc_status hc_ep_finish_peer(hc_ep_t p, const void* const* w_ranks, void* z, void* stream);
+
 /* ---- Applications built on the hot path ------------------------------ */
 
 /* f4: PMF of the difference X - Y of independent random vectors with Bernoulli axes

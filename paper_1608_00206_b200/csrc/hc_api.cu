@@ -721,6 +721,41 @@ extern "C" hc_status hc_ep_local(hc_ep_t p, const void* x, const void* y, void* 
   return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
 }
 
+extern "C" hc_status hc_ep_finish_peer(hc_ep_t p, const void* const* w_ranks, void* z, void* stream) {
+  if (!p || !w_ranks || !z) return HC_ERR_NULL;
+  if (p->ngpu > 8) return HC_ERR_SHARD;
+  EPPeer pe{};
+  const uint64_t np = upow3(p->k);
+  for (int r = 0; r < p->ngpu; ++r) {
+    if (!w_ranks[r]) return HC_ERR_NULL;
+    pe.w[r] = w_ranks[r];
+    uint64_t e0, e1, c0, c1;
+    hc_ep_range(p->D, p->k, p->ngpu, r, &e0, &e1, &c0, &c1);
+    for (uint64_t e = e0; e < e1; ++e) {
+      pe.own[e] = (uint8_t)r;
+      pe.base[e] = (uint32_t)(e - e0);
+    }
+  }
+  (void)np;
+  const uint64_t ncols = p->c1 - p->c0, nct = upow3(p->D - p->k);
+  if (ncols == 0) return HC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned g = (unsigned)((ncols + 127) / 128);
+  LaunchScope ls("ep_inverse_peer", st);
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    switch (p->k) {
+      case 1: ep_top_inverse_peer<T, 1><<<g, 128, 0, st>>>(pe, (T*)z, ncols, nct, p->c0); break;
+      case 2: ep_top_inverse_peer<T, 2><<<g, 128, 0, st>>>(pe, (T*)z, ncols, nct, p->c0); break;
+      case 3: ep_top_inverse_peer<T, 3><<<g, 128, 0, st>>>(pe, (T*)z, ncols, nct, p->c0); break;
+      default: ep_top_inverse_peer<T, 4><<<g, 128, 0, st>>>(pe, (T*)z, ncols, nct, p->c0); break;
+    }
+  };
+  if (p->dtype == HC_INT64) go(uint64_t{});
+  else go(double{});
+  return cudaGetLastError() == cudaSuccess ? HC_OK : HC_ERR_CUDA;
+}
+
 extern "C" hc_status hc_ep_finish(hc_ep_t p, const void* wt, void* z, void* stream) {
   if (!p || !wt || !z) return HC_ERR_NULL;
   cudaError_t e = p->dtype == HC_INT64

@@ -44,4 +44,28 @@ __global__ void __launch_bounds__(128) ep_top_inverse(const T* __restrict__ wt, 
   for (int e = 0; e < NP; ++e) st_cs(z + (uint64_t)e * ncols + col, v[e]);
 }
 
+// f3: the same interpolation reading each evaluation point straight from the buffer of the
+// rank that owns it (peer memory on a multi-GPU node) -- no gathered copy.  own[e] = owner
+// rank of point e, base[e] = (e - e_begin of the owner) * ncols_total, col0 = this rank's
+// first column.
+struct EPPeer {
+  const void* w[8];
+  uint8_t own[81];
+  uint32_t base[81];
+};
+template <class T, int K>
+__global__ void __launch_bounds__(128) ep_top_inverse_peer(EPPeer pe, T* __restrict__ z, uint64_t ncols,
+                                                           uint64_t ncols_total, uint64_t col0) {
+  const uint64_t col = (uint64_t)blockIdx.x * 128 + threadIdx.x;
+  if (col >= ncols) return;
+  constexpr int NP = ipow3(K);
+  T v[NP];
+#pragma unroll
+  for (int e = 0; e < NP; ++e)
+    v[e] = ((const T*)pe.w[pe.own[e]])[(uint64_t)pe.base[e] * ncols_total + col0 + col];
+  inv_reg<K, T>(v);
+#pragma unroll
+  for (int e = 0; e < NP; ++e) st_cs(z + (uint64_t)e * ncols + col, v[e]);
+}
+
 }  // namespace hc

@@ -44,6 +44,7 @@ _lib.hc_ep_create.argtypes = [ctypes.POINTER(_P), _I, _I, _I, _I, _I]
 _lib.hc_ep_destroy.argtypes = [_P]
 _lib.hc_ep_local.argtypes = [_P, _P, _P, _P, _P]
 _lib.hc_ep_finish.argtypes = [_P, _P, _P, _P]
+_lib.hc_ep_finish_peer.argtypes = [_P, ctypes.POINTER(_P), _P, _P]
 _lib.hc_convolve_difference.argtypes = [_P, _P, _P, _P, _P]
 _lib.hc_carries_work_len.argtypes = [_I]
 _lib.hc_carries_work_len.restype = _U64
@@ -281,6 +282,17 @@ class EPPlan:
                              _P(_stream_ptr(stream))), "hc_ep_local")
         return w
 
+    def finish_peer(self, w_ranks, z, stream=None):
+        """hc_ep_finish_peer: interpolation reading every rank's w directly
+        (w_ranks: one device tensor per rank -- peer-mapped buffers on a multi-GPU node)."""
+        if len(w_ranks) != self.ngpu:
+            raise ValueError("need one w buffer per rank")
+        arr = (_P * self.ngpu)(*[_P(t.data_ptr()) for t in w_ranks])
+        m = self.npoints * (self.c1 - self.c0)
+        _ok(_lib.hc_ep_finish_peer(self._h, arr, _dev(z, m, self.dtype_code, "z"), _P(_stream_ptr(stream))),
+            "hc_ep_finish_peer")
+        return z
+
     def finish(self, wt, z, stream=None):
         m = self.npoints * (self.c1 - self.c0)
         _ok(_lib.hc_ep_finish(self._h, _dev(wt, m, self.dtype_code, "wt"), _dev(z, m, self.dtype_code, "z"),
@@ -322,6 +334,20 @@ def ep_exchange(w, wt, D: int, k: int, rank: int, world: int, dist=None):
         for req in dist.batch_isend_irecv(ops):
             req.wait()
     return wt
+
+
+def ep_peer_buffers(w, rank: int, world: int, dist=None):
+    """f3: every rank's hc_ep_local output as a device tensor this process can read -- its own
+    buffer, and CUDA IPC mappings of the others' (torch tensor reductions; lazy peer access,
+    i.e. NVLink reads on a multi-GPU node).  Call once per buffer; the mappings stay valid
+    while the owners keep their tensors."""
+    if world == 1 or dist is None:
+        return [w]
+    from torch.multiprocessing.reductions import reduce_tensor
+    mine = reduce_tensor(w)
+    objs = [None] * world
+    dist.all_gather_object(objs, mine)
+    return [w if r == rank else f(*a) for r, (f, a) in enumerate(objs)]
 
 
 def launch_count() -> int:

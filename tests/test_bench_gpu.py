@@ -49,6 +49,7 @@ def test_bench_two_ranks_share_one_gpu():
 
 @pytest.mark.parametrize("args,parallelism", [
     (["--workload", "c3_d16_i64", "--variant", "evalpoint", "--ep-k", "2"], "evalpoint k=2 x2 (all-to-all)"),
+    (["--workload", "c3_d16_i64", "--variant", "evalpoint-peer", "--ep-k", "2"], "evalpoint k=2 x2 (peer reads)"),
     (["--workload", "c5_d22_f64", "--steps", "1", "--no-cpu-baseline"],
      "8 output-split shards streamed through one buffer, 4 per rank x2"),
 ])

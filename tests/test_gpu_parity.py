@@ -282,6 +282,15 @@ def test_evalpoint_variant_emulated_ranks(hc, orc, D, k, dtype, nranks):
         torch.cuda.synchronize()
         got.reshape(npnt, nc)[:, p.c0:p.c1] = z.view(npnt, -1).cpu().numpy()
     _assert_close(got, want, x, y)
+    # f3: the exchange fused into the interpolation -- every rank reads the owners' buffers
+    ws = [W[p.e0:p.e1].contiguous().view(-1) for p in plans]
+    got2 = np.empty(3 ** D, dtype=want.dtype)
+    for p in plans:
+        z = torch.empty(npnt * (p.c1 - p.c0), dtype=tdt, device="cuda")
+        p.finish_peer(ws, z)
+        torch.cuda.synchronize()
+        got2.reshape(npnt, nc)[:, p.c0:p.c1] = z.view(npnt, -1).cpu().numpy()
+    assert np.array_equal(got2, got)
     if nranks == 1:  # world 1: ep_exchange is the identity copy
         p = plans[0]
         w = torch.empty(npnt * nc, dtype=tdt, device="cuda")
