@@ -69,6 +69,33 @@ __global__ void __launch_bounds__(T8_NT, 2) k_pairs(int iters, double* sink) {
   if (s == 1234.5) *sink = s;
 }
 
+// dedicated roles: warps 0-7 run F2 only (243 units), warps 8-10 run F1 only (e_s = w - 8),
+// one CTA per SM, a barrier per pair among all 11 warps
+__global__ void __launch_bounds__(352, 1) k_roles(int iters, double* sink) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sm = reinterpret_cast<double*>(smem_raw);
+  double* P = sm;
+  double* R = sm + T8Cfg<double>::ALIAS;
+  for (int i = threadIdx.x; i < T8Cfg<double>::ALIAS + T8_NRAW * RS_SZ; i += 352) sm[i] = 1e-3 * (i % 97);
+  __syncthreads();
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const bool unit = tid < 243;
+  const int uu = t8_unit(tid < 256 ? tid : 0);
+  const int ea2 = uu / 81, eS = uu - 81 * ea2;
+  double acc[27];
+#pragma unroll
+  for (int i = 0; i < 27; ++i) acc[i] = 0;
+  for (int p = 0; p < iters; ++p) {
+    if (w >= 8) t8_f1<double>(R + (p % T8_NRAW) * RS_SZ, P + ((p + 1) & 1) * PS_SZ, w - 8, lane);
+    else if (unit) t8_f2<double>(P + (p & 1) * PS_SZ, ea2, eS, acc);
+    __syncthreads();
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 27; ++i) s += acc[i];
+  if (s == 1234.5) *sink = s;
+}
+
 template <int MODE>
 float run(int grid, int iters, double* sink) {
   auto k = k_pairs<MODE>;
@@ -104,6 +131,21 @@ int main() {
       const double clk_per = (ms * 1e-3) * (clk * 1e3) / ((double)iters * ctas);
       printf("ctas/SM %d %-12s %.3f ms  %.0f clk per pair-iteration per SM\n", ctas, names[m], ms, clk_per);
     }
+  }
+  {
+    cudaFuncSetAttribute(k_roles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T8Cfg<double>::SMEM);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_roles<<<sms, 352, T8Cfg<double>::SMEM>>>(iters, sink);
+    cudaEventRecord(e0);
+    k_roles<<<sms, 352, T8Cfg<double>::SMEM>>>(iters, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("1 CTA/SM, 8 F2 warps + 3 F1 warps: %.3f ms  %.0f clk per pair-iteration per SM\n", ms,
+           (ms * 1e-3) * (clk * 1e3) / (double)iters);
   }
   printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
