@@ -368,7 +368,8 @@ tile8_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z
   ring_init(raw_bar);
   RawRing rr{raw_bar, 0, 0};
   const int k = D - 8;
-  const uint64_t pol_in = policy_evict_last();
+  // a single pair's slices are reused by many tiles (keep them in L2); a batch's are read once
+  const uint64_t pol_in = nitems > nslab ? policy_evict_first() : policy_evict_last();
   if (threadIdx.x == T8_SCHED) {
     pf.left = 0;
     pf.pos = 0xffffffffu;  // next() moves to position 0

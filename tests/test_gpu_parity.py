@@ -462,3 +462,35 @@ def test_warp_specialised_variants(var):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("D", [3, 9, 11, 13, 15])
+def test_int64_full_range_wraparound(hc, orc, D):
+    # inputs over the whole 64-bit range: every product and every interpolation wraps; the
+    # pipeline is a ring homomorphism mod 2^64 (R3), so it must agree bit for bit
+    # with Algorithm 1 computed mod 2^64 -- through the single-level, two-level and batched
+    # engines, a shard, and the differences entry point
+    x = hcgen.splitmix64(8800 + D, 0, 1 << D).view(np.int64)
+    y = hcgen.splitmix64(8800 + D, 1, 1 << D).view(np.int64)
+    want = orc.conv(x, y)
+    got = _run(hc, x, y).cpu().numpy()
+    assert np.array_equal(got, want)
+    xb = np.stack([x, y])
+    yb = np.stack([y, x])
+    zb = torch.empty((2, 3 ** D), dtype=torch.int64, device="cuda")
+    hc.convolve_batched(_gpu(xb), _gpu(yb), zb)
+    torch.cuda.synchronize()
+    assert np.array_equal(zb.cpu().numpy(), orc.conv_batched(xb, yb))
+    if D >= 15:
+        p = hc.Plan(D, "int64", 2, 1)
+        b, e = p.shard_info()
+        zs = torch.empty(e - b, dtype=torch.int64, device="cuda")
+        p.convolve_sharded(_gpu(x), _gpu(y), zs)
+        torch.cuda.synchronize()
+        assert np.array_equal(zs.cpu().numpy(), want[b:e])
+    zd = torch.empty(3 ** D, dtype=torch.int64, device="cuda")
+    hc.Plan(D, "int64").convolve_difference(_gpu(x), _gpu(y), zd)
+    torch.cuda.synchronize()
+    mask = (1 << D) - 1
+    yf = y[np.bitwise_xor(np.arange(1 << D), mask)]
+    assert np.array_equal(zd.cpu().numpy(), orc.conv(x, yf))
