@@ -339,7 +339,7 @@ struct hc_plan_s {
   void* xu = nullptr;             // two-level: middle-axes-evaluated input slices (prep kernel)
   void* yu = nullptr;
   std::mutex order_mu;
-  std::map<std::pair<uint64_t, uint64_t>, uint32_t*> orders;  // [u0,u1) -> device processing order
+  std::map<std::pair<uint64_t, uint64_t>, uint4*> orders;  // [u0,u1) -> device processing order
   // host entry point workspace
   void* dx = nullptr;
   void* dy = nullptr;
@@ -463,7 +463,7 @@ extern "C" hc_status hc_shard_info(hc_plan_t p, int rank, uint64_t* zb, uint64_t
 // Processing order of the slabs [u0, u1) for the slab engine: sorted by the number of
 // direct-split pairs 2^{#1(t_T)} so that consecutive slabs cost the same and a pass-2 item
 // rarely waits for a slow pass-1 item of its slab.  Cached per range on the plan.
-static const uint32_t* slab_order(hc_plan_t p, uint64_t u0, uint64_t u1) {
+static const uint4* slab_order(hc_plan_t p, uint64_t u0, uint64_t u1) {
   std::lock_guard<std::mutex> lk(p->order_mu);
   auto key = std::make_pair(u0, u1);
   auto it = p->orders.find(key);
@@ -480,11 +480,20 @@ static const uint32_t* slab_order(hc_plan_t p, uint64_t u0, uint64_t u1) {
     v[i] = {ones, (uint32_t)i};
   }
   std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-  std::vector<uint32_t> h(n);
-  for (uint64_t i = 0; i < n; ++i) h[i] = v[i].second;
-  uint32_t* d = nullptr;
-  if (cudaMalloc(&d, sizeof(uint32_t) * n) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-  if (cudaMemcpy(d, h.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice) != cudaSuccess) {
+  std::vector<uint4> h(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    // trit split of the top index (PAPER.md 173-177): digit 2 -> base bit, digit 1 -> free bit
+    uint64_t t = u0 + v[i].second;
+    uint32_t base = 0, freeb = 0;
+    for (int a = 0; a < p->g.k; ++a, t /= 3) {
+      if (t % 3 == 2) base |= 1u << a;
+      else if (t % 3 == 1) freeb |= 1u << a;
+    }
+    h[i] = make_uint4(v[i].second, base, freeb, 0);
+  }
+  uint4* d = nullptr;
+  if (cudaMalloc(&d, sizeof(uint4) * n) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  if (cudaMemcpy(d, h.data(), sizeof(uint4) * n, cudaMemcpyHostToDevice) != cudaSuccess) {
     cudaFree(d);
     return nullptr;
   }
@@ -501,7 +510,7 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
   if (!g.two_level) {
     e = launch_any(p->dtype, x, y, z, p->D, u0, g.nunits, u1 - u0, st);
   } else {
-    const uint32_t* order = slab_order(p, u0, u1);
+    const uint4* order = slab_order(p, u0, u1);
     if (!order) return HC_ERR_CAPACITY;
     static const int dbg = getenv("HC_DEBUG_SKIP") ? atoi(getenv("HC_DEBUG_SKIP")) : 0;
     static const int lag = getenv("HC_SLAB_LAG") ? atoi(getenv("HC_SLAB_LAG")) : 1;
@@ -524,15 +533,15 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
       cudaMemcpyFromSymbolAsync(h, hc_phase, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
       double tot = 0;
-      for (int i = 0; i < 7; ++i) tot += (double)h[i];
+      for (int i : {0, 1, 4, 5, 6}) tot += (double)h[i];
       if (getenv("HC_SLAB_WS") && atoi(getenv("HC_SLAB_WS")))
         fprintf(stderr, "ws phase (Mclk, CTA sum): compute: throttle %.0f pairloop %.0f S-wait %.0f handoff %.0f | "
                 "epilogue: tiles %.0f p2 %.0f idle %.0f\n", h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6,
                 h[4] / 1e6, h[5] / 1e6, h[6] / 1e6);
       else
       fprintf(stderr, "phase(Mclk/CTA-sum): select+wait %.0f pairloop %.0f inv+store %.0f p2 %.0f end %.0f "
-              "(tot %.0f) | F1 mbar wait %.0f\n", h[0] / 1e6, h[1] / 1e6, h[6] / 1e6, h[4] / 1e6, h[5] / 1e6,
-              tot / 1e6, h[7] / 1e6);
+              "(tot %.0f) | F1 mbar wait %.0f | t224 select %.0f end %.0f\n", h[0] / 1e6, h[1] / 1e6, h[6] / 1e6,
+              h[4] / 1e6, h[5] / 1e6, tot / 1e6, h[7] / 1e6, h[2] / 1e6, h[3] / 1e6);
     }
 #endif
   }

@@ -144,6 +144,8 @@ __device__ __forceinline__ long long* ph_sh() {
 #define PH_MARK(i) do { if (threadIdx.x == 128) { long long t_ = clock64(); ph_sh()[i] += t_ - ph_sh()[8]; ph_sh()[8] = t_; } } while (0)
 #define PH_WAIT_BEGIN(c) long long phw_ = (c) ? clock64() : 0
 #define PH_WAIT_END(c) do { if (c) atomicAdd((unsigned long long*)&ph_sh()[7], (unsigned long long)(clock64() - phw_)); } while (0)
+#define PH_T0 long long pht0_ = clock64()
+#define PH_T1(i) atomicAdd((unsigned long long*)&ph_sh()[i], (unsigned long long)(clock64() - pht0_))
 #define PH_FLUSH do { if (threadIdx.x == 128) for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&hc_phase[i_], (unsigned long long)ph_sh()[i_]); } while (0)
 #else
 #define PH_DECL do { } while (0)
@@ -151,6 +153,8 @@ __device__ __forceinline__ long long* ph_sh() {
 #define PH_WAIT_BEGIN(c) do { } while (0)
 #define PH_WAIT_END(c) do { } while (0)
 #define PH_FLUSH do { } while (0)
+#define PH_T0 do { } while (0)
+#define PH_T1(i) do { } while (0)
 #endif
 
 // ---- raw-slice staging ring and the cross-item prefetcher -----------------------------
@@ -445,16 +449,18 @@ __device__ __forceinline__ ItemDec decode_item(uint32_t q, uint32_t ns, uint32_t
 #endif
 constexpr int T8_QN = HC_QN;  // claimed items held per CTA
 constexpr uint32_t T8_EXH = 0xffffffffu;
+constexpr int T8_DEFER = -2;  // s_sel: selection postponed past the item's closing barrier
 #ifndef HC_P2CH
 #define HC_P2CH 3
 #endif
 constexpr int T8_P2CH = HC_P2CH;  // 9-column chunks per pass-2 item
 
-struct Slot {
-  uint32_t q;            // claim index, T8_EXH = past the end
-  uint32_t p1, j, r, loc;
-  uint32_t base, freeb;  // pass 1: trit split of the slab's top index
+struct __align__(16) Slot {
+  uint32_t loc, base, freeb, pad;  // = order[j] (16 B): slab offset; pass 1: trit split of its top index
+  uint32_t q;                      // claim index, T8_EXH = past the end (or being decoded)
+  uint32_t p1, j, r;
 };
+static_assert(T8_QN == 3, "the scheduler packs the slots' claim indices into one uint4");
 
 template <class T, int M>
 __global__ void __launch_bounds__(T8_NT, 2)
@@ -465,6 +471,8 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   __shared__ Slot s_slot[T8_QN];
+  __shared__ uint4 s_qm;  // {q of slots 0..2, mask of pass-1 slots}: one load for the selection
+  __shared__ uint4 s_jm;  // {j of slots 0..2, -}
   __shared__ int s_sel;
   __shared__ __align__(8) uint64_t raw_bar[T8_NRAW];
   __shared__ Prefetch pf;
@@ -485,8 +493,8 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
     if (q >= total) { o.q = T8_EXH; return; }
     const ItemDec d = decode_item(q, ns, N1, N2, lag);
     o.q = q; o.p1 = d.p1; o.j = d.j; o.r = d.r;
-    o.loc = args.order[d.j];
-    if (d.p1) trit_split(args.slab0 + o.loc, args.k, o.base, o.freeb);
+    const uint4 oi = args.order[d.j];
+    o.loc = oi.x; o.base = oi.y; o.freeb = oi.z;
   };
   // prefetch cursor: pass-1 slots in claim order (pf.pos = claim index of the cursor item)
   auto next = [&](Prefetch& c) -> bool {
@@ -522,73 +530,108 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
     }
   };
 
+  // Thread T8_SCHED's state.  The slots live in shared memory (few registers are free in the
+  // pair loop); s_qm / s_jm mirror their claim indices, kinds and slabs so that the selection,
+  // which the whole CTA waits for, is two shared loads and register logic.
+  auto set_meta = [&](int i, uint32_t q, bool p1, uint32_t j) {
+    uint32_t* qm = reinterpret_cast<uint32_t*>(&s_qm);
+    qm[i] = q;
+    qm[3] = p1 ? (qm[3] | 1u << i) : (qm[3] & ~(1u << i));
+    reinterpret_cast<uint32_t*>(&s_jm)[i] = j;
+  };
   if (threadIdx.x == T8_SCHED) {
     uint32_t c[T8_QN];
     for (int i = 0; i < T8_QN; ++i) c[i] = atomicAdd(args.ctr, 1u);
-    for (int i = 0; i < T8_QN; ++i) decode(c[i], s_slot[i]);
+    s_qm.w = 0;
+    for (int i = 0; i < T8_QN; ++i) {
+      decode(c[i], s_slot[i]);
+      set_meta(i, s_slot[i].q, s_slot[i].q != T8_EXH && s_slot[i].p1, s_slot[i].j);
+    }
     pf.left = 0;
     pf.pos = T8_EXH;
   }
-  // thread 0, kept across one item so that global-memory latencies overlap the item:
-  uint32_t cv[T8_QN];          // slab-completion counters of the pass-2 slots (loaded at item start)
-  uint32_t cmask = 0;          // slots whose cv[] is valid
-  int pslot = -1;              // slot whose claim is being decoded: claim index pq, order value ov
-  uint32_t pq = 0, pov = 0;
-  ItemDec pd{};
-  PH_DECL;
-  while (true) {
-    if (threadIdx.x == T8_SCHED) {
-      auto finish_pending = [&]() {  // complete the claim decoded one item ago
-        Slot& o = s_slot[pslot];
-        o.q = pq; o.p1 = pd.p1; o.j = pd.j; o.r = pd.r; o.loc = pov;
-        if (pd.p1) trit_split(args.slab0 + pov, args.k, o.base, o.freeb);
-        pslot = -1;
-      };
-      int sel, p2w;
-      for (int pass = 0;; ++pass) {
-        int p2r = -1, p1 = -1;
-        p2w = -1;
-        for (int i = 0; i < T8_QN; ++i) {
-          const Slot& o = s_slot[i];
-          if (i == pslot || o.q == T8_EXH) continue;
-          if (o.p1) {
-            if (p1 < 0 || o.q < s_slot[p1].q) p1 = i;
-          } else if (skip2 || (((cmask >> i) & 1) && cv[i] >= N1)) {
-            if (p2r < 0 || o.q < s_slot[p2r].q) p2r = i;
-          } else if (p2w < 0 || o.q < s_slot[p2w].q) {
-            p2w = i;
-          }
+  // kept across one item so that global-memory latencies overlap the item:
+  uint32_t cv[T8_QN];  // slab-completion counters of the pass-2 slots (loaded at item start)
+  uint32_t cmask = 0;  // slots whose cv[] is valid
+  int pslot = -1;      // slot whose claim pq is being decoded (its order[] entry is in flight)
+  uint32_t pq = 0;
+  auto finish_pending = [&]() {  // complete the claim decoded one item ago
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    Slot& o = s_slot[pslot];
+    o.q = pq;
+    set_meta(pslot, pq, o.p1, o.j);
+    pslot = -1;
+  };
+  // Selection of the next item (thread T8_SCHED); result in s_sel.  Before the item's closing
+  // barrier (may_wait = false) the tile just computed cannot be published yet (other warps'
+  // stores may be in flight), so a selection that would wait or leave returns T8_DEFER and is
+  // redone after the barrier, where signal() is safe.
+  auto select_next = [&](bool may_wait) {
+    PH_T0;
+    int sel, p2w;
+    uint32_t jw = 0;
+    for (int pass = 0;; ++pass) {
+      const uint4 qm = s_qm, jm = s_jm;
+      const uint32_t rq[3] = {qm.x, qm.y, qm.z}, rj[3] = {jm.x, jm.y, jm.z};
+      int p2r = -1, p1 = -1;
+      uint32_t q1 = T8_EXH, q2r = T8_EXH, q2w = T8_EXH;
+      p2w = -1;
+#pragma unroll
+      for (int i = 0; i < T8_QN; ++i) {
+        if (i == pslot || rq[i] == T8_EXH) continue;
+        if ((qm.w >> i) & 1) {
+          if (rq[i] < q1) { q1 = rq[i]; p1 = i; }
+        } else if (skip2 || (((cmask >> i) & 1) && cv[i] >= N1)) {
+          if (rq[i] < q2r) { q2r = rq[i]; p2r = i; }
+        } else if (rq[i] < q2w) {
+          q2w = rq[i]; p2w = i; jw = rj[i];
         }
-        sel = p2r >= 0 ? p2r : (p1 >= 0 ? p1 : p2w);
-        // before waiting (or leaving), the pending claim must be visible: it may be the
-        // pass-1 item everybody waits for
-        if ((sel < 0 || sel == p2w) && pslot >= 0 && pass == 0) {
-          finish_pending();
-          continue;
-        }
-        break;
       }
-      if (sel >= 0 && sel == p2w) {  // nothing else to do: signal, then wait for the slab
-        signal();
-        pump();
-        const uint32_t j = s_slot[sel].j;
-        while (ld_relaxed(done_ctr + j) < N1) __nanosleep(64);
+      sel = p2r >= 0 ? p2r : (p1 >= 0 ? p1 : p2w);
+      // before waiting (or leaving), the pending claim must be visible: it may be the
+      // pass-1 item everybody waits for
+      if ((sel < 0 || sel == p2w) && pslot >= 0 && pass == 0) {
+        finish_pending();
+        continue;
       }
-      if (sel < 0) signal();
-      s_sel = sel;
+      break;
     }
-    __syncthreads();
-    const int sel = s_sel;
+    if (!may_wait && (sel < 0 || sel == p2w)) {
+      s_sel = T8_DEFER;
+      return;
+    }
+    if (sel >= 0 && sel == p2w) {  // nothing else to do: signal, then wait for the slab
+      signal();
+      pump();
+      while (ld_relaxed(done_ctr + jw) < N1) __nanosleep(64);
+    }
+    if (sel < 0) signal();
+    s_sel = sel;
+    PH_T1(2);
+  };
+  PH_DECL;
+  if (threadIdx.x == T8_SCHED) select_next(true);
+  __syncthreads();
+  while (true) {
+    const int sel = *(volatile int*)&s_sel;
     if (sel < 0) break;
-    const Slot it = s_slot[sel];
+    Slot it;  // read now: thread T8_SCHED rewrites the slot before this item's last barrier
+    {
+      const volatile uint32_t* src = reinterpret_cast<const volatile uint32_t*>(&s_slot[sel]);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(&it);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[i] = src[i];
+    }
     uint32_t claim = 0;
     if (threadIdx.x == T8_SCHED) {
       claim = atomicAdd(args.ctr, 1u);  // refills slot `sel` after this item
       cmask = 0;                         // snapshot the other pass-2 slots' slabs (used next time)
+      const uint4 qm = s_qm, jm = s_jm;
+      const uint32_t rq[3] = {qm.x, qm.y, qm.z}, rj[3] = {jm.x, jm.y, jm.z};
+#pragma unroll
       for (int i = 0; i < T8_QN; ++i) {
-        const Slot& o = s_slot[i];
-        if (i != sel && i != pslot && o.q != T8_EXH && !o.p1) {
-          cv[i] = ld_relaxed(done_ctr + o.j);  // non-blocking; compared at the next selection
+        if (i != sel && i != pslot && rq[i] != T8_EXH && !((qm.w >> i) & 1)) {
+          cv[i] = ld_relaxed(done_ctr + rj[i]);  // non-blocking; compared at the next selection
           cmask |= 1u << i;
         }
       }
@@ -598,6 +641,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
     if (it.p1) {
       if (skip1) {
         if (threadIdx.x == T8_SCHED) atomicAdd(done_ctr + it.j, 1u);
+        __syncthreads();  // everybody has read s_sel and the slot
       } else {
         tile8<T, false>(1 << __popc(it.freeb), zs + (uint64_t)it.r * 6561ull, sm, rr, pol_keep, pump, signal);
         PH_MARK(6);
@@ -607,7 +651,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       // barrier): the reads below are ordered after it by that control dependency and the
       // barrier, and go to L2 (.cg), where the producers' fenced stores already are
       if (threadIdx.x == T8_SCHED) pump();
-      // three 9-column chunks per item (a third as many items to schedule)
+      // three 9-column chunks per item (a third as many items to schedule), pipelined
 #pragma unroll 1
       for (int ch = 0; ch < T8_P2CH; ++ch) {
         if (ch) __syncthreads();  // the exchange buffer is rewritten by the next chunk
@@ -616,24 +660,35 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       }
       PH_MARK(4);
     }
-    __syncthreads();  // the item's smem is free
+    // thread T8_SCHED, once its share of the item is done: bookkeeping and the selection of
+    // the next item, overlapping the other warps' tails (every thread has read s_sel and the
+    // slot before the item's first barrier)
     if (threadIdx.x == T8_SCHED) {
+      PH_T0;
       if (it.p1 && !skip1) pend = it.j;  // published during the next item (or before a wait)
-      if (pslot >= 0) {                  // finish the claim decoded one item ago
-        Slot& o = s_slot[pslot];
-        o.q = pq; o.p1 = pd.p1; o.j = pd.j; o.r = pd.r; o.loc = pov;
-        if (pd.p1) trit_split(args.slab0 + pov, args.k, o.base, o.freeb);
-        pslot = -1;
-      }
-      // start decoding this item's replacement: the order[] load completes during the next item
-      if (claim >= total) {
-        s_slot[sel].q = T8_EXH;
-      } else {
+      if (pslot >= 0) finish_pending();  // the claim decoded one item ago
+      // start decoding this item's replacement into its slot (invisible until finished: q =
+      // T8_EXH); its order[] entry is copied by cp.async during the next item
+      Slot& o = s_slot[sel];
+      o.q = T8_EXH;
+      set_meta(sel, T8_EXH, false, 0);
+      if (claim < total) {
+        const ItemDec d = decode_item(claim, ns, N1, N2, lag);
+        o.p1 = d.p1; o.j = d.j; o.r = d.r;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&o.loc)),
+                     "l"(args.order + d.j) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
         pslot = sel;
         pq = claim;
-        pd = decode_item(claim, ns, N1, N2, lag);
-        pov = args.order[pd.j];
       }
+      PH_T1(3);
+      select_next(false);
+    }
+    __syncthreads();  // the item's smem is free; s_sel is set
+    if (*(volatile int*)&s_sel == T8_DEFER) {
+      __syncthreads();  // everybody has seen T8_DEFER before it is overwritten
+      if (threadIdx.x == T8_SCHED) select_next(true);
+      __syncthreads();
     }
     PH_MARK(5);
   }

@@ -265,7 +265,8 @@ struct SlabArgs {
   uint32_t nslab;      // slabs in this launch
   int k;               // top axes
   uint32_t* ctr;       // [0] = work counter, [1 + j] = pass-1 tiles done in slab j
-  const uint32_t* order;  // processing position j -> slab offset within the launch (cost-sorted)
+  const uint4* order;  // processing position j -> {slab offset within the launch, base, freeb, 0}:
+                       // cost-sorted, with the trit split of the slab's top index precomputed
   int debug_skip;      // timing experiments only (HC_DEBUG_SKIP): 1 = no pass 2, 2 = no pass 1
   uint32_t lag;        // pass 2 of slab j is scheduled after pass 1 of slab j + lag (>= 1)
 };

@@ -114,7 +114,7 @@ slabws_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict_
     auto dec = [&](uint32_t q, uint32_t& j, uint32_t& r, uint32_t& base, uint32_t& freeb) {
       j = q / N1;
       r = q - j * N1;
-      trit_split(args.slab0 + args.order[j], args.k, base, freeb);
+      base = args.order[j].y, freeb = args.order[j].z;
     };
     // prefetch cursor over the queued claims (claim order = processing order)
     uint32_t head = 0;  // WS_CLEAD only
@@ -159,7 +159,7 @@ slabws_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict_
           dec(q, j, r, base, freeb);
           s_citem[1] = base;
           s_citem[2] = freeb;
-          s_citem[3] = args.order[j];
+          s_citem[3] = args.order[j].x;
           // throttle: slab j's pass 1 starts once slab j - lag has been finished by pass 2
           if (j >= lag && ld_relaxed(p2done + (j - lag)) < N2) {
             pump();
@@ -264,7 +264,7 @@ slabws_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict_
         s_ejob[0] = kind;
         s_ejob[1] = j;
         s_ejob[2] = c;
-        s_ejob[3] = kind == 2 ? args.order[j] : 0;
+        s_ejob[3] = kind == 2 ? args.order[j].x : 0;
         if (kind == 2) q2 = T8_EXH;
       }
       bar_named(WS_BAR_E, 256);
