@@ -799,13 +799,27 @@ unsigned ew_grid(uint64_t n) {
 }
 template <class T, int L>
 cudaError_t carry_tile(const T* z, T* part, uint64_t ntiles, cudaStream_t st) {
-  const size_t sm = 2 * sizeof(T) * (size_t)ipow3(L);
-  auto k = carry_tile_kernel<T, L>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
-  LaunchScope ls("carry", st);
-  k<<<(unsigned)ntiles, 256, sm, st>>>(z, part);
-  return cudaGetLastError();
+  if constexpr (L == 8) {
+    const size_t sm = sizeof(T) * (size_t)(6561 + 243 * 15 + 81 * 31);
+    auto k = carry_tile8_kernel<T>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t grid = ntiles < 2ull * nsm ? ntiles : 2ull * nsm;
+    LaunchScope ls("carry", st);
+    k<<<(unsigned)grid, 256, sm, st>>>(z, part, ntiles);
+    return cudaGetLastError();
+  } else {
+    const size_t sm = 2 * sizeof(T) * (size_t)ipow3(L);
+    auto k = carry_tile_kernel<T, L>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    LaunchScope ls("carry", st);
+    k<<<(unsigned)ntiles, 256, sm, st>>>(z, part);
+    return cudaGetLastError();
+  }
 }
 // one global combining step for axis c (compile-time c, 32-bit indices when they fit)
 template <class T, int C>

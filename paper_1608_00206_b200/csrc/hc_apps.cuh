@@ -79,6 +79,56 @@ __global__ void __launch_bounds__(256) carry_tile_kernel(const T* __restrict__ z
   for (uint32_t v = threadIdx.x; v < V; v += 256) part[t * V + v] = res[v];
 }
 
+// Persistent form for L = 8 (D >= 8): the next tile's z values are loaded into registers
+// (coalesced, 26 per thread) while the current tile is combined, so the HBM read overlaps
+// the shared-memory steps; axes 0-2 are combined in registers (a row of 27 values -> 15
+// partial sums v = k0 + 2 k1 + 4 k2), axes 3-7 in shared memory (carry_tile_steps from C = 3).
+// Shared memory: raw tile 3^8 + 243 x 15 + 81 x 31 elements (2 CTAs per SM).
+template <class T>
+__global__ void __launch_bounds__(256, 2) carry_tile8_kernel(const T* __restrict__ z, T* __restrict__ part,
+                                                             uint64_t ntiles) {
+  constexpr int N = 6561, NL = (N + 255) / 256;
+  extern __shared__ __align__(128) unsigned char carry_smem[];
+  T* raw = reinterpret_cast<T*>(carry_smem);
+  T* b1 = raw + N;          // [243][15]
+  T* b2 = b1 + 243 * 15;    // [81][31]
+  const int tid = threadIdx.x;
+  T r[NL];
+  auto load = [&](uint64_t t) {
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (tid + 256 * j < N) r[j] = z[t * N + tid + 256 * j];
+  };
+  uint64_t t = blockIdx.x;
+  if (t < ntiles) load(t);
+  for (; t < ntiles; t += gridDim.x) {
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (tid + 256 * j < N) raw[tid + 256 * j] = r[j];
+    __syncthreads();
+    if (t + gridDim.x < ntiles) load(t + gridDim.x);  // in flight during the steps below
+    if (tid < 243) {
+      T v[27], b[15];
+#pragma unroll
+      for (int k = 0; k < 27; ++k) v[k] = raw[27 * tid + k];
+#pragma unroll
+      for (int k = 0; k < 15; ++k) b[k] = T(0);
+#pragma unroll
+      for (int k2 = 0; k2 < 3; ++k2)
+#pragma unroll
+        for (int k1 = 0; k1 < 3; ++k1)
+#pragma unroll
+          for (int k0 = 0; k0 < 3; ++k0) b[k0 + 2 * k1 + 4 * k2] = Ar<T>::add(b[k0 + 2 * k1 + 4 * k2], v[k0 + 3 * k1 + 9 * k2]);
+#pragma unroll
+      for (int k = 0; k < 15; ++k) b1[15 * tid + k] = b[k];
+    }
+    __syncthreads();
+    carry_tile_steps<T, 8, 3>(b1, b2);  // c = 3..7, result (511 values) in b2
+    for (int v = tid; v < 511; v += 256) part[t * 511 + v] = b2[v];
+    __syncthreads();  // b1 / b2 / raw are rewritten by the next tile
+  }
+}
+
 // one further axis C in global memory: A [nr][2^(C+1) - 1] -> B [nr / 3][2^(C+2) - 1]
 template <class T, class I, int C>
 __global__ void __launch_bounds__(256) carry_step_kernel(const T* __restrict__ A, T* __restrict__ B, uint64_t nr2) {
@@ -118,25 +168,35 @@ __global__ void __launch_bounds__(256) pnorm_pre_kernel(const double* __restrict
 }
 
 // z[k] = max x * max y * z[k]^(1/p), optionally rounded to the nearest integer; p = 2^sq:
-// sq square roots
+// sq square roots.  Four independent elements per thread and iteration: one load in flight
+// per thread cannot cover HBM latency at 2048 threads per SM.
+__device__ __forceinline__ double pnorm_root(double v, double s, double ip, int sq, int round_to_int) {
+  if (v > 0.0) {
+    if (sq >= 0) {
+      for (int k = 0; k < sq; ++k) v = sqrt(v);
+    } else {
+      v = pow(v, ip);
+    }
+    v *= s;
+  } else {
+    v = 0.0;
+  }
+  return round_to_int ? rint(v) : v;
+}
 __global__ void __launch_bounds__(256) pnorm_post_kernel(double* __restrict__ z, uint64_t n, double p, int sq,
                                                          const unsigned long long* mx, int round_to_int) {
   const double s = __longlong_as_double((long long)mx[0]) * __longlong_as_double((long long)mx[1]);
   const double ip = 1.0 / p;
-  for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256) {
-    double v = z[i];
-    if (v > 0.0) {
-      if (sq >= 0) {
-        for (int k = 0; k < sq; ++k) v = sqrt(v);
-      } else {
-        v = pow(v, ip);
-      }
-      v *= s;
-    } else {
-      v = 0.0;
-    }
-    z[i] = round_to_int ? rint(v) : v;
+  const uint64_t stride = (uint64_t)gridDim.x * 256;
+  uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = z[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) z[i + u * stride] = pnorm_root(v[u], s, ip, sq, round_to_int);
   }
+  for (; i < n; i += stride) z[i] = pnorm_root(z[i], s, ip, sq, round_to_int);
 }
 
 }  // namespace hc
