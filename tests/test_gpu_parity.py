@@ -494,3 +494,25 @@ def test_int64_full_range_wraparound(hc, orc, D):
     mask = (1 << D) - 1
     yf = y[np.bitwise_xor(np.arange(1 << D), mask)]
     assert np.array_equal(zd.cpu().numpy(), orc.conv(x, yf))
+
+
+def test_max_dimension_d24_shard(hc, orc):
+    # HC_MAX_D = 24 (3^24 = 2.8e11 entries, 2.3 TB of output): one shard of a 128-way output
+    # split, int64 (bit-exact), sampled cells plus the shard's first and last tiles
+    D, n, r = 24, 128, 77
+    x = hcgen.uniform_int(2424, 0, 1 << D, 0, 255)
+    y = hcgen.uniform_int(2424, 1, 1 << D, 0, 255)
+    p = hc.Plan(D, "int64", n, r)
+    b, e = p.shard_info()
+    assert 0 < e - b < 3 ** D // 64
+    zs = torch.empty(e - b, dtype=torch.int64, device="cuda")
+    p.convolve_sharded(_gpu(x), _gpu(y), zs)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(24)
+    loc = np.unique(np.concatenate([rng.integers(0, e - b, 3000), np.arange(0, 3 ** 8),
+                                    np.arange(e - b - 3 ** 8, e - b)]))
+    got = zs[torch.from_numpy(loc).cuda()].cpu().numpy()
+    want = orc.conv_cells(x, y, (loc + b).astype(np.uint64))
+    assert np.array_equal(got, want)
+    p.close()
+    del zs
