@@ -128,6 +128,18 @@ hc_status check_device() {
   return ok ? HC_OK : HC_ERR_DEVICE;
 }
 
+// Per-device launch caches: kernel attributes (dynamic shared memory size) and occupancy are
+// set / queried once per device, so one process may drive several GPUs.
+constexpr int kMaxDev = 64;
+inline int& dev_slot(int* cache, int& scratch) {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDev) {
+    scratch = 0;
+    return scratch;  // no caching: recomputed on every call
+  }
+  return cache[d];
+}
+
 // ---- 8-axis tiles: single level (tile8_kernel) and two levels (prep + slab8_kernel) ----
 // persistent grid size for a T8 kernel: SMs x resident CTAs per SM
 template <class K>
@@ -153,7 +165,9 @@ cudaError_t launch_tile8(const T* x, const T* y, T* z, int D, uint64_t slab0, ui
   static const int ws = getenv("HC_TILE_WS") ? atoi(getenv("HC_TILE_WS")) : 0;
   if (ws) {
     auto kern = tilews_kernel<T>;
-    static int grid_max = 0;
+    static int gm_cache[kMaxDev] = {};
+    int gm_scratch = 0;
+    int& grid_max = dev_slot(gm_cache, gm_scratch);
     if (!grid_max) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TWSCfg::SMEM);
       if (e != cudaSuccess) return e;
@@ -171,7 +185,9 @@ cudaError_t launch_tile8(const T* x, const T* y, T* z, int D, uint64_t slab0, ui
     return cudaGetLastError();
   }
   auto kern = tile8_kernel<T>;
-  static int grid_max = 0;
+  static int gm_cache[kMaxDev] = {};
+  int gm_scratch = 0;
+  int& grid_max = dev_slot(gm_cache, gm_scratch);
   cudaError_t e = t8_grid(kern, grid_max);
   if (e != cudaSuccess) return e;
   const unsigned grid = (unsigned)(nitems < (uint64_t)grid_max ? nitems : (uint64_t)grid_max);
@@ -183,7 +199,9 @@ cudaError_t launch_tile8(const T* x, const T* y, T* z, int D, uint64_t slab0, ui
 template <class T, int M>
 cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st) {
   auto kern = slab8_kernel<T, M>;
-  static int grid_max = 0;
+  static int gm_cache[kMaxDev] = {};
+  int gm_scratch = 0;
+  int& grid_max = dev_slot(gm_cache, gm_scratch);
   cudaError_t e = t8_grid(kern, grid_max);
   if (e != cudaSuccess) return e;
   const uint64_t items = (uint64_t)a.nslab * (upow3(M) + upow3(8) / (P2W * T8_P2CH));
@@ -206,7 +224,9 @@ cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const Sla
 template <class T, int M>
 cudaError_t launch_slabws_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st) {
   auto kern = slabws_kernel<T, M>;
-  static int grid_max = 0;
+  static int gm_cache[kMaxDev] = {};
+  int gm_scratch = 0;
+  int& grid_max = dev_slot(gm_cache, gm_scratch);
   if (!grid_max) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSCfg<T, M>::SMEM);
     if (e != cudaSuccess) return e;
@@ -257,11 +277,13 @@ cudaError_t launch_tile_cfg(const T* x, const T* y, T* z, int D, uint64_t slab0,
                             uint64_t nitems, cudaStream_t st) {
   using Cfg = TileCfg<T, C, B, A>;
   auto kern = tile_kernel<T, C, B, A>;
-  static bool attr_set = false;  // per instantiation
+  static int attr_cache[kMaxDev] = {};  // per instantiation and device
+  int attr_scratch = 0;
+  int& attr_set = dev_slot(attr_cache, attr_scratch);
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set = 1;
   }
   const uint64_t maxgrid = 0x7fffffffull;
   for (uint64_t off = 0; off < nitems; off += maxgrid) {
