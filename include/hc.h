@@ -28,8 +28,12 @@
  * Errors: every function returns hc_status; nothing throws across the ABI.  D must be in
  *   [1, HC_MAX_D] (D = 0 is rejected; the paper's recursion bottoms out at D = 1,
  *   PAPER.md 255-263).
- * Thread safety: plans are immutable after creation except for the host-buffer entry
- *   point's workspace; do not call hc_convolve_host on one plan from two threads at once.
+ * Thread safety / concurrency: a plan holds device state that its calls reuse -- the slab
+ *   engine's work and completion counters (D >= 13), the scratch of the application entry
+ *   points and the host-buffer entry point's workspace.  Calls on ONE plan must therefore be
+ *   ordered (one stream, or streams ordered by events); to run convolutions concurrently on
+ *   several streams or threads, create one plan per stream.  Plans of different devices are
+ *   independent (create each with its device current).
  */
 #ifndef HC_H
 #define HC_H
