@@ -107,6 +107,11 @@ def _stream_ptr(stream):
 def _dev(t, n, dtype_code, name):
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor")
+    import torch
+    cur = torch.cuda.current_device()
+    if t.device.index != cur:
+        raise ValueError(f"{name} is on {t.device} but the current device is cuda:{cur} "
+                         "(plans and launches use the current device)")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
     if t.numel() != n:
