@@ -48,6 +48,24 @@ __device__ __forceinline__ void fwd_reg(const T* in, T* out) {
   }
 }
 
+// fwd_reg with each output stored as soon as it is formed (dst[e * stride]): the evaluation
+// tree is walked depth first, so at most N partial sums per level are live instead of all
+// 3^N outputs (register pressure of the callers that also hold accumulators)
+template <int N, int STRIDE, class T>
+__device__ __forceinline__ void fwd_store(const T* in, T* dst) {
+  if constexpr (N == 0) {
+    dst[0] = in[0];
+  } else {
+    constexpr int h = 1 << (N - 1), m = ipow3(N - 1);
+    fwd_store<N - 1, STRIDE, T>(in, dst);                  // e_top = 0  <- a0
+    T s[h];
+#pragma unroll
+    for (int i = 0; i < h; ++i) s[i] = Ar<T>::add(in[i], in[i + h]);
+    fwd_store<N - 1, STRIDE, T>(s, dst + m * STRIDE);      // e_top = 1  <- a0 + a1
+    fwd_store<N - 1, STRIDE, T>(in + h, dst + 2 * m * STRIDE);  // e_top = 2  <- a1
+  }
+}
+
 // acc[e] += fwd(x)[e] * fwd(y)[e] for all e in {0,1,2}^N without materialising fwd(x):
 // the paper's recursion shape (Algorithm 2) on evaluation points, with the
 // inputs left intact.

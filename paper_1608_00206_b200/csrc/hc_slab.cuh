@@ -203,11 +203,8 @@ __device__ __forceinline__ void t8_f1(const T* R, T* P, int es, int lane) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) in[j] = Ar<T>::add(src[8 * j], src[RS_H1 + 8 * j]);
   }
-  T out[27];
-  fwd_reg<3, T>(in, out);
   T* dst = P + op * PS_OP + ba2 * PS_A2 + (27 * es) * PS_ROW + bc;
-#pragma unroll
-  for (int e = 0; e < 27; ++e) dst[e * PS_ROW] = out[e];
+  fwd_store<3, PS_ROW, T>(in, dst);
 }
 
 // Stage F2 of one pair: thread (e_a2, e_S) loads its 8 + 8 base values (summing the two
