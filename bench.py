@@ -433,10 +433,29 @@ def main():
     alg_bytes_per_launch = (out_bytes_local + in_bytes_local * max(launches_per_step, 1)) / max(launches_per_step, 1)
     peak, peak_src = load_peaks()
     achieved = alg_bytes_per_launch / (k_avg / 1e3) / 1e9 if k_avg > 0 else None
+    traffic = load_traffic(wl)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": load_traffic(wl),
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": prof_name, "alg_bytes_per_launch": alg_bytes_per_launch, "launch_ms": k_avg,
-                "peak_source": peak_src}
+                "peak_source": peak_src,
+                # the same efficiency against the 8.0 TB/s spec figure, and the
+                # DRAM traffic ncu measured for this launch (profiles/ncu_traffic.json) over its time
+                "frac_vs_spec_8000": (achieved / 8000.0) if achieved else None,
+                "dram_gbs": (traffic / (k_avg / 1e3) / 1e9) if (traffic and k_avg > 0) else None}
+    # fp64 co-roofline of the two-level engine (DESIGN.md §4 cost model): algorithmic fp64
+    # instructions per output entry = pair loop (F2 27 FMA + 38 add per unit and pair, 16 row
+    # sums on the e_a2 = 1 units, F1 19 adds (+8) per lane) x (4/3)^k pairs + 2/3 per
+    # interpolated axis (tile and middle axes); against the measured DADD/DFMA lane rate
+    co = None
+    if tdt == torch.float64 and prof_name == "slab" and D >= 13:
+        k_top = D - 14 if D >= 14 else 0
+        pair_ops = (243 * (27 + 38) + 81 * 16 + 96 * 19 + 32 * 8) / 6561.0
+        ops_per_out = pair_ops * (4.0 / 3.0) ** k_top + (2.0 / 3.0) * min(D, 14)
+        ops = ops_per_out * n_local / max(launches_per_step, 1)
+        fp64_peak = 17.5e12  # fp64 lane-instructions/s measured on this B200 (DFMA 17.0, DADD 18.5 T/s)
+        co = {"bound": "fp64", "ops_per_output": ops_per_out, "achieved": ops / (k_avg / 1e3) / 1e12 if k_avg else None,
+              "peak": fp64_peak / 1e12, "unit": "T fp64 instr-lanes/s",
+              "frac": (ops / (k_avg / 1e3) / fp64_peak) if k_avg else None}
 
     # end to end through the host-buffer C-ABI entry point (pinned host memory, copies inside)
     e2e = None
@@ -483,7 +502,7 @@ def main():
                               % (n_total * 8 / 1e9)),
                        "min_bytes_per_step": n_total * 8 + in_bytes},
             "hbm_gbs_min_bytes": (n_total * 8 + in_bytes) / (ms_per_step / 1e3) / 1e9,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "co_roofline": co, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
