@@ -14,3 +14,6 @@ run c5_d22_streamed --workload c5_d22_f64 --steps 3 --warmup 3
 run c4_d20_evalpoint_k4 --workload c4_d20_f64 --variant evalpoint --steps 5
 run c4_d20_evalpoint_peer_k4 --workload c4_d20_f64 --variant evalpoint-peer --steps 5
 run f4_difference_d20_f64 --workload f4_difference_d20_f64 --steps 5
+run f1_conv1d_d20_i64 --workload f1_conv1d_d20_i64 --steps 3
+run f2_maxconv_d20_f64 --workload f2_maxconv_d20_f64 --steps 3
+run c4_d20 --workload c4_d20_f64 --steps 10
