@@ -516,3 +516,14 @@ def test_max_dimension_d24_shard(hc, orc):
     assert np.array_equal(got, want)
     p.close()
     del zs
+
+
+def test_c_example_program(tmp_path):
+    # examples/hc_example.c: a plain C program using the ABI (host-buffer entry point) and
+    # checking D = 10 against the definition by brute force
+    import subprocess
+    from test_lib_cpu import _build_example
+    exe = _build_example(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 of 59049 output entries differ" in r.stdout

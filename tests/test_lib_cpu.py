@@ -121,3 +121,28 @@ def test_ep_ranges_partition(hc, D, k):
         hc.ep_range(D, k, 3 ** k + 1, 0)
     with pytest.raises(hc.HCError):
         hc.ep_range(D, 5, 1, 0)
+
+
+def _build_example(tmp_path):
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_1608_00206_b200")
+    exe = str(tmp_path / "hc_example")
+    subprocess.check_call(["gcc", "-O2", "-Wall", "-Wextra", "-Werror", "-std=c99", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "examples", "hc_example.c"), "-L", libdir, "-lhc",
+                           f"-Wl,-rpath,{libdir}", "-o", exe])
+    return exe
+
+
+def test_c_example_builds_against_the_header(tmp_path):
+    # the boundary is plain C: the example compiles with gcc -std=c99 -Werror and links
+    # against libhc.so; without a GPU it must fail loudly (no CPU fallback)
+    import subprocess
+    exe = _build_example(tmp_path)
+    import torch
+    if not torch.cuda.is_available():
+        r = subprocess.run([exe], capture_output=True, text=True)
+        assert r.returncode == 1 and "no usable CUDA device" in r.stderr
