@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const T* __restrict__ x, cons
 #ifdef HC_PHASE_PROF
 __device__ unsigned long long hc_phase[16];
 __device__ __forceinline__ long long* ph_sh() {
-  __shared__ long long s_ph[10];  // [0..7] phase sums, [8] thread-0 timestamp, [9] wait start
+  __shared__ long long s_ph[10];  // [0..7] phase sums, [8] timestamp of the marking thread, [9] wait start
   return s_ph;
 }
 #define PH_DECL do { if (threadIdx.x == 128) { for (int i_ = 0; i_ < 8; ++i_) ph_sh()[i_] = 0; ph_sh()[8] = clock64(); } } while (0)
@@ -160,11 +160,11 @@ __device__ __forceinline__ long long* ph_sh() {
 // ---- raw-slice staging ring and the cross-item prefetcher -----------------------------
 // T8_NRAW stages; stage n is filled by 4 TMA copies (x and y, two 128-element halves each)
 // and completes on its mbarrier.  `done` counts fills consumed by F1 (advanced identically
-// in every thread); `seq` (thread 0) counts fills issued.  Fill n may be issued once fill
+// in every thread); `seq` (the scheduling thread T8_SCHED) counts fills issued.  Fill n may be issued once fill
 // n - T8_NRAW has been read, i.e. seq - done < T8_NRAW at a point after a barrier.
 struct RawRing {
   uint64_t* bar;     // [T8_NRAW] in shared memory
-  uint32_t seq;      // fills issued so far (thread 0)
+  uint32_t seq;      // fills issued so far (T8_SCHED)
   uint32_t done;     // fills consumed so far
 };
 template <class T>
@@ -241,7 +241,7 @@ __device__ __forceinline__ void t8_f2(const T* P, int ea2, int eS, T* acc) {
   fwd_mul_acc<3, T>(xt, yt, acc);
 }
 
-// Prefetch cursor (shared memory, thread 0 only) over the pairs of the pass-1 items in the
+// Prefetch cursor (shared memory, T8_SCHED only) over the pairs of the pass-1 items in the
 // order the CTA will consume them.  Pair p of an item has subset s_p of freeb (ascending
 // subsets, PAPER.md 173-177 direct split): i_T = base | s_p, j_T = base | (freeb & ~s_p).
 struct Prefetch {
@@ -253,7 +253,7 @@ struct Prefetch {
   uint32_t pos;    // position of the cursor item in the CTA's item sequence
 };
 
-// Fill the ring (thread 0).  next(pf) advances the cursor to the next pass-1 item the CTA
+// Fill the ring (T8_SCHED).  next(pf) advances the cursor to the next pass-1 item the CTA
 // will run (setting sx0, sy0, stride, base, freeb, s = 0, left) or returns false.
 template <class T, class Next>
 __device__ __forceinline__ void pf_pump(Prefetch& pf, RawRing& rr, T* R, uint64_t pol, Next&& next) {
@@ -405,9 +405,10 @@ tile8_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z
 
 // Two-level persistent kernel: pass-1 items (slab j, e_U) and pass-2 items (slab j, 9
 // columns) from one work counter in the order P1(0) P1(1) P2(0) P1(2) P2(1) ...; slabs in
-// cost order (args.order).  Each CTA holds T8_QN claimed items ("slots"), decoded by
-// thread 0 when the claim returns.  Selection: a pass-2 item whose slab is complete
-// (lowest claim first), else the lowest pass-1 item, else wait for the lowest pass-2 item.
+// cost order (args.order).  Each CTA holds T8_QN claimed items ("slots"), decoded by the
+// scheduling thread T8_SCHED when the claim returns.  Selection: a pass-2 item whose slab is
+// complete (lowest claim first), else the lowest pass-1 item, else wait for the lowest pass-2
+// item.
 // Pass-1 items therefore run in claim order, which is the order the prefetcher issues
 // their slices.  Deadlock freedom: pass-1 items wait for nothing; a pass-2 item waits only
 // for pass-1 items of its slab, all claimed earlier.  The earliest unfinished claim is
@@ -485,7 +486,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   T* R = sm + T8Cfg<T>::ALIAS;
   uint32_t* done_ctr = args.ctr + 1;
 
-  // thread-0 helpers ------------------------------------------------------------------
+  // T8_SCHED helpers -------------------------------------------------------------------
   auto decode = [&](uint32_t q, Slot& o) {
     if (q >= total) { o.q = T8_EXH; return; }
     const ItemDec d = decode_item(q, ns, N1, N2, lag);
@@ -515,10 +516,10 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
     return true;
   };
   auto pump = [&]() { pf_pump<T>(pf, rr, R, pol_in, next); };
-  uint32_t pend = T8_EXH;  // thread 0: slab position of a finished, not yet signalled tile
+  uint32_t pend = T8_EXH;  // T8_SCHED: slab position of a finished, not yet signalled tile
   // Completion of a pass-1 tile is published with a gpu-scope fence (cumulative over the
   // CTA's stores, which precede it through a CTA barrier) and an atomic increment.  Called
-  // where thread 0 has no global stores in flight (mid item, before a wait, at exit).
+  // where T8_SCHED has no global stores in flight (mid item, before a wait, at exit).
   auto signal = [&]() {
     if (pend != T8_EXH) {
       __threadfence();
