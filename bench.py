@@ -298,11 +298,9 @@ def main():
         n_local = n_total = 3 ** D
         if w["app"] == "conv1d":
             out1 = torch.empty((2 << D) - 1, dtype=tdt, device="cuda")
-            work = torch.empty(hc.carries_work_len(D), dtype=tdt, device="cuda")
 
-            def step():
-                app_plan.convolve(xg, yg, z)
-                hc.apply_carries(D, z, out1, work)
+            def step():  # hc_conv1d: int64 at D >= 13 fuses the carries into pass 2
+                hc.conv1d(xg, yg, out1, plan=app_plan, z_work=z)
         elif w["app"] == "maxconv":
             def step():
                 app_plan.maxconv_pnorm(xg, yg, z, 16.0)

@@ -160,6 +160,18 @@ hc_status hc_convolve_difference(hc_plan_t plan, const void* x, const void* y, v
 uint64_t hc_carries_work_len(int D);
 hc_status hc_apply_carries(int D, hc_dtype dtype, const void* z, void* out, void* work, void* stream);
 
+/* Ordinary 1-D convolution out[m] = sum_i x[i] y[m - i], m < 2^(D+1) - 1, of two length-2^D
+ * vectors: the carry-free (hypercube) convolution of their bit-axis embeddings followed by the
+ * carries (PAPER.md 354-373).  plan: single-GPU plan of dimension D and the vectors' dtype.
+ * z_work: 3^D elements (device workspace); out: 2^(D+1) - 1 elements (device, overwritten).
+ * work: hc_carries_work_len(D) elements, or NULL for int64 plans with D >= 13 -- there the
+ * carries are fused into the slab engine's pass 2 (every final z[k] is added into
+ * out[sum_b k_b 2^b] with exact wrapping uint64 atomics), z_work only holds the pass-1 tiles
+ * and z itself is never written.  fp64 and D < 13 run hc_convolve then hc_apply_carries.
+ * Errors: HC_ERR_SHARD for a multi-rank plan; otherwise as hc_convolve. */
+hc_status hc_conv1d(hc_plan_t plan, const void* x, const void* y, void* z_work, void* out, void* work,
+                    void* stream);
+
 /* f2: p-norm max-convolution (PAPER.md 341-352), fp64 plans only.  x, y >= 0 (2^D each):
  *     z[k] = mx * my * ( sum_{i+j=k} (x[i]/mx)^p (y[j]/my)^p )^(1/p),   mx = max x, my = max y,
  * which lies in [M, n_k^(1/p) M] for the max-convolution M = max_{i+j=k} x[i] y[j] and the

@@ -11,6 +11,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/hc.h"
@@ -196,9 +197,9 @@ cudaError_t launch_tile8(const T* x, const T* y, T* z, int D, uint64_t slab0, ui
   return cudaGetLastError();
 }
 
-template <class T, int M>
+template <class T, int M, int EPI = 0>
 cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st) {
-  auto kern = slab8_kernel<T, M>;
+  auto kern = slab8_kernel<T, M, EPI>;
   static int gm_cache[kMaxDev] = {};
   int gm_scratch = 0;
   int& grid_max = dev_slot(gm_cache, gm_scratch);
@@ -256,6 +257,15 @@ cudaError_t launch_slabws_m(const T* x, const T* y, T* z, T* xu, T* yu, const Sl
 
 template <class T>
 cudaError_t launch_slab8(const T* x, const T* y, T* z, T* xu, T* yu, int M, const SlabArgs& a, cudaStream_t st) {
+  if constexpr (std::is_same<T, uint64_t>::value) {
+    if (a.cout) {  // f1: carries fused into pass 2
+      switch (M) {
+        case 5: return launch_slab8_m<T, 5, 2>(x, y, z, xu, yu, a, st);
+        case 6: return launch_slab8_m<T, 6, 2>(x, y, z, xu, yu, a, st);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+  }
   static const int ws = getenv("HC_SLAB_WS") ? atoi(getenv("HC_SLAB_WS")) : 0;
   if (ws) {
     switch (M) {
@@ -525,7 +535,7 @@ static const uint4* slab_order(hc_plan_t p, uint64_t u0, uint64_t u1) {
 
 // units [u0, u1) of the plan's geometry into z (z points at unit u0)
 static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, uint64_t u0, uint64_t u1,
-                           cudaStream_t st, int slot) {
+                           cudaStream_t st, int slot, unsigned long long* cout = nullptr) {
   if (u1 <= u0) return HC_OK;
   const Geometry& g = p->g;
   cudaError_t e;
@@ -536,7 +546,7 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
     if (!order) return HC_ERR_CAPACITY;
     static const int dbg = getenv("HC_DEBUG_SKIP") ? atoi(getenv("HC_DEBUG_SKIP")) : 0;
     static const int lag = getenv("HC_SLAB_LAG") ? atoi(getenv("HC_SLAB_LAG")) : 1;
-    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg, (uint32_t)(lag < 1 ? 1 : lag)};
+    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg, (uint32_t)(lag < 1 ? 1 : lag), cout};
 #ifdef HC_PHASE_PROF
     {
       unsigned long long zero[16] = {0};
@@ -908,6 +918,25 @@ extern "C" hc_status hc_apply_carries(int D, hc_dtype dtype, const void* z, void
                       ? apply_carries_t<uint64_t>(D, (const uint64_t*)z, (uint64_t*)out, (uint64_t*)work, (cudaStream_t)stream)
                       : apply_carries_t<double>(D, (const double*)z, (double*)out, (double*)work, (cudaStream_t)stream);
   return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
+}
+
+extern "C" hc_status hc_conv1d(hc_plan_t p, const void* x, const void* y, void* z_work, void* out, void* work,
+                               void* stream) {
+  if (!p || !x || !y || !z_work || !out) return HC_ERR_NULL;
+  if (!aligned16(x) || !aligned16(y) || !aligned8(z_work) || !aligned8(out)) return HC_ERR_ALIGN;
+  if (p->ngpu != 1) return HC_ERR_SHARD;
+  const int D = p->D;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->dtype == HC_INT64 && p->g.two_level) {
+    // the slab engine adds every final z[k] into out[val(k)] (uint64, exact in any order);
+    // z_work only holds the pass-1 tiles
+    if (cudaMemsetAsync(out, 0, sizeof(uint64_t) * ((2ull << D) - 1), st) != cudaSuccess) return HC_ERR_CUDA;
+    return run_range(p, x, y, z_work, 0, p->g.nunits, st, 0, (unsigned long long*)out);
+  }
+  if (D > 8 && !work) return HC_ERR_NULL;
+  hc_status s = run_range(p, x, y, z_work, 0, p->g.nunits, st, 0);
+  if (s != HC_OK) return s;
+  return hc_apply_carries(D, p->dtype, z_work, out, work, stream);
 }
 
 extern "C" hc_status hc_convolve_difference(hc_plan_t p, const void* x, const void* y, void* z, void* stream) {

@@ -453,6 +453,94 @@ constexpr int T8_DEFER = -2;  // s_sel: selection postponed past the item's clos
 #endif
 constexpr int T8_P2CH = HC_P2CH;  // 9-column chunks per pass-2 item
 
+// f1, carries fused into pass 2 (int64 only: wrapping uint64 sums are exact in any order).
+// One 9-column chunk of a slab: round 1 as in p2_item; round 2 interpolates the HI middle
+// axes and, instead of storing z, adds every final value z[k] into out[val(k)],
+// val(k) = sum_b k_b 2^b (PAPER.md 354-373: the carry-free digits of the 1-D convolution).
+// Within the chunk val = base + a(pos) + 256 (val3(e_lo) + 8 valHI(e_hi)), a = k0 + 2 k1;
+// the sums are reduced over e_hi in registers, over e_lo in shared memory, and each of the
+// chunk's distinct bins (a, u) gets one global atomic add.  `mid` runs on thread `sched`
+// after the loads (as in p2_item).
+template <int N>
+__device__ __forceinline__ constexpr int bitval3(int e) {  // sum_b digit_b(e) 2^b, N base-3 digits
+  int v = 0;
+  for (int b = 0, p = 1; b < N; ++b, p <<= 1, e /= 3) v += (e % 3) * p;
+  return v;
+}
+template <class T, int M, class Mid>
+__device__ __forceinline__ void p2_carry_chunk(const T* __restrict__ zs, uint32_t c, T* sm, int task,
+                                               unsigned long long* __restrict__ out, uint64_t base, int sched,
+                                               Mid&& mid) {
+  using Q = P2Cfg<M>;
+  constexpr int LO = Q::LO, HI = Q::HI, NLO = Q::NLO, NHI = Q::NHI, P2S = Q::P2S;
+  static_assert(LO == 3, "three low middle axes");
+  constexpr int NB = (2 << HI) - 1;          // distinct valHI(e_hi)
+  constexpr int NU = 15 + 8 * (NB - 1);      // u = val3(e_lo) + 8 valHI in [0, NU)
+  constexpr uint64_t ROW = 6561;
+  const uint64_t col0 = (uint64_t)c * P2W;
+  // round 1: task (e_hi, pos) loads its 27 column entries, interpolates the LO axes
+  if (task >= 0)
+    for (int w = task; w < NHI * P2W; w += 243) {
+      const int eh = w / P2W, pos = w - eh * P2W;
+      T v[NLO];
+#pragma unroll
+      for (int e = 0; e < NLO; ++e) v[e] = ld_cg(zs + (uint64_t)(eh * NLO + e) * ROW + col0 + pos);
+      inv_reg<LO, T>(v);
+#pragma unroll
+      for (int e = 0; e < NLO; ++e) sm[eh * P2S + e * P2W + pos] = v[e];
+    }
+  __syncthreads();
+  if ((int)threadIdx.x == sched) mid();
+  // round 2: task (e_lo, pos) interpolates the HI axes and sums its values by valHI(e_hi)
+  T b[NB];
+  const bool t2 = task >= 0 && task < NLO * P2W;
+  const int el = task / P2W, pos = task - el * P2W;
+  if (t2) {
+    T v[NHI];
+#pragma unroll
+    for (int e = 0; e < NHI; ++e) v[e] = sm[e * P2S + el * P2W + pos];
+    inv_reg<HI, T>(v);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) b[i] = T(0);
+#pragma unroll
+    for (int e = 0; e < NHI; ++e) b[bitval3<HI>(e)] += v[e];
+  }
+  __syncthreads();  // the exchange is reused below
+  T* bs = sm;                    // [pos][vhi][e_lo]: 9 x NB x 27
+  T* cs = sm + 9 * NB * NLO;     // [pos][vhi][val3(e_lo)]: 9 x NB x 15
+  if (t2) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) bs[(pos * NB + i) * NLO + el] = b[i];
+  }
+  __syncthreads();
+  // sum over e_lo by val3(e_lo): thread (pos, vhi)
+  for (int t = threadIdx.x; t < 9 * NB; t += blockDim.x) {
+    T cc[15];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) cc[i] = T(0);
+#pragma unroll
+    for (int e = 0; e < NLO; ++e) cc[bitval3<3>(e)] += bs[t * NLO + e];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) cs[t * 15 + i] = cc[i];
+  }
+  __syncthreads();
+  // final bins (a, u): a = k0 + 2 k1 over the positions with that value, u = w + 8 vhi
+  for (int t = threadIdx.x; t < 7 * NU; t += blockDim.x) {
+    const int a = t / NU, u = t - a * NU;
+    T sum = T(0);
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+      if ((p % 3) + 2 * (p / 3) != a) continue;
+#pragma unroll
+      for (int vh = 0; vh < NB; ++vh) {
+        const int w = u - 8 * vh;
+        if (w >= 0 && w < 15) sum += cs[(p * NB + vh) * 15 + w];
+      }
+    }
+    atomicAdd(out + base + a + 256 * (uint64_t)u, (unsigned long long)sum);
+  }
+}
+
 struct __align__(16) Slot {
   uint32_t loc, base, freeb, pad;  // = order[j] (16 B): slab offset; pass 1: trit split of its top index
   uint32_t q;                      // claim index, T8_EXH = past the end (or being decoded)
@@ -460,7 +548,7 @@ struct __align__(16) Slot {
 };
 static_assert(T8_QN == 3, "the scheduler packs the slots' claim indices into one uint4");
 
-template <class T, int M>
+template <class T, int M, int EPI = 0>  // EPI 2: carries fused into pass 2 (f1, uint64 only)
 __global__ void __launch_bounds__(T8_NT, 2)
 slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__ z, SlabArgs args) {
   constexpr uint32_t N1 = (uint32_t)ipow3(M);
@@ -650,11 +738,32 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       // barrier, and go to L2 (.cg), where the producers' fenced stores already are
       if (threadIdx.x == T8_SCHED) pump();
       // three 9-column chunks per item (a third as many items to schedule), pipelined
+      if constexpr (EPI == 2) {
+        // carry bins: val(k) = (tile digits) + 2^8 (middle digits) + 2^(8+M) (top digits)
+        uint64_t vtop = 0;
+        {
+          uint64_t t = args.slab0 + it.loc;
+          for (int b = 0; b < args.k; ++b, t /= 3) vtop += (t % 3) << b;
+        }
+#pragma unroll 1
+        for (int ch = 0; ch < T8_P2CH; ++ch) {
+          if (ch) __syncthreads();  // the exchange buffer is rewritten by the next chunk
+          const uint32_t cc = it.r * T8_P2CH + ch;  // chunk = tile digits k2..k7
+          uint64_t vcol = 0;
+          {
+            uint32_t t = cc;
+            for (int b = 2; b < 8; ++b, t /= 3) vcol += (uint64_t)(t % 3) << b;
+          }
+          p2_carry_chunk<T, M>(zs, cc, sm, threadIdx.x < 243 ? (int)threadIdx.x : -1, args.cout,
+                               vcol + (vtop << (8 + M)), ch == 0 ? T8_SCHED : -1, signal);
+        }
+      } else {
 #pragma unroll 1
       for (int ch = 0; ch < T8_P2CH; ++ch) {
         if (ch) __syncthreads();  // the exchange buffer is rewritten by the next chunk
         p2_item<T, M, 8>(zs, it.r * T8_P2CH + ch, sm, threadIdx.x < 243 ? (int)threadIdx.x : -1,
                          ch == 0 ? T8_SCHED : -1, signal, [] { __syncthreads(); });
+      }
       }
       PH_MARK(4);
     }

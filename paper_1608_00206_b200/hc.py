@@ -49,6 +49,7 @@ _lib.hc_convolve_difference.argtypes = [_P, _P, _P, _P, _P]
 _lib.hc_carries_work_len.argtypes = [_I]
 _lib.hc_carries_work_len.restype = _U64
 _lib.hc_apply_carries.argtypes = [_I, _I, _P, _P, _P, _P]
+_lib.hc_conv1d.argtypes = [_P, _P, _P, _P, _P, _P, _P]
 _lib.hc_maxconv_pnorm.argtypes = [_P, _P, _P, _P, ctypes.c_double, _I, _P]
 _lib.hc_launch_count.restype = _U64
 _lib.hc_prof_enable.argtypes = [_I]
@@ -233,18 +234,26 @@ def apply_carries(D: int, z, out, work=None, stream=None):
     return out
 
 
-def conv1d(x, y, out=None, plan=None, stream=None):
+def conv1d(x, y, out=None, plan=None, stream=None, z_work=None):
     """Ordinary 1-D convolution of two length-2^D CUDA vectors through the carry-free
-    (hypercube) convolution and the carries (PAPER.md 354-373)."""
+    (hypercube) convolution and the carries (hc_conv1d, PAPER.md 354-373); int64 with
+    D >= 13 fuses the carries into the slab engine."""
     import torch
     n = x.numel()
     D = n.bit_length() - 1
     plan = plan or Plan(D, x.dtype)
-    z = torch.empty(3 ** D, dtype=x.dtype, device=x.device)
-    plan.convolve(x, y, z, stream)
+    code = _dtype_code(x.dtype)
+    if z_work is None:
+        z_work = torch.empty(3 ** D, dtype=x.dtype, device=x.device)
     if out is None:
         out = torch.empty((2 << D) - 1, dtype=x.dtype, device=x.device)
-    return apply_carries(D, z, out, stream=stream)
+    fused = code == HC_INT64 and D >= 13
+    wl = carries_work_len(D)
+    work = None if (fused or wl == 0) else torch.empty(wl, dtype=x.dtype, device=x.device)
+    _ok(_lib.hc_conv1d(plan._h, _dev(x, n, code, "x"), _dev(y, n, code, "y"), _dev(z_work, 3 ** D, code, "z_work"),
+                       _dev(out, (2 << D) - 1, code, "out"), _P(work.data_ptr()) if work is not None else _P(0),
+                       _P(_stream_ptr(stream))), "hc_conv1d")
+    return out
 
 
 def ep_range(D: int, k: int, ngpu: int, rank: int):

@@ -336,7 +336,7 @@ def test_difference_pmf(hc, apps, D, dtype):
     _assert_close(z.cpu().numpy(), apps.difference_pmf(x, y), x, y)
 
 
-@pytest.mark.parametrize("D", [1, 4, 8, 9, 11, 14])
+@pytest.mark.parametrize("D", [1, 4, 8, 9, 11, 13, 14, 15])
 def test_conv1d_via_carries_int64(hc, D):
     # f1: carry-free convolution + carries = the ordinary 1-D convolution (numpy's definition)
     x = hcgen.uniform_int(9200 + D, 0, 1 << D, -10 ** 6, 10 ** 6)
@@ -527,3 +527,20 @@ def test_c_example_program(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 of 59049 output entries differ" in r.stdout
+
+
+@pytest.mark.parametrize("D", [13, 16])
+def test_conv1d_fused_equals_convolve_then_carries(hc, D):
+    # int64, D >= 13: hc_conv1d fuses the carries into pass 2 (atomics into the bins); it must
+    # equal the unfused route (hc_convolve, then hc_apply_carries) bit for bit, including
+    # values that wrap
+    x = hcgen.splitmix64(7700 + D, 0, 1 << D).view(np.int64)
+    y = hcgen.splitmix64(7700 + D, 1, 1 << D).view(np.int64)
+    xg, yg = _gpu(x), _gpu(y)
+    fused = hc.conv1d(xg, yg)
+    z = torch.empty(3 ** D, dtype=torch.int64, device="cuda")
+    hc.Plan(D, "int64").convolve(xg, yg, z)
+    ref = torch.empty((2 << D) - 1, dtype=torch.int64, device="cuda")
+    hc.apply_carries(D, z, ref)
+    torch.cuda.synchronize()
+    assert torch.equal(fused, ref)
