@@ -299,7 +299,7 @@ def main():
         if w["app"] == "conv1d":
             out1 = torch.empty((2 << D) - 1, dtype=tdt, device="cuda")
 
-            def step():  # hc_conv1d: int64 at D >= 13 fuses the carries into pass 2
+            def step():  # hc_conv1d: int64 at D >= 13 fuses the carries into pass 2, tiles in z
                 hc.conv1d(xg, yg, out1, plan=app_plan, z_work=z)
         elif w["app"] == "maxconv":
             def step():

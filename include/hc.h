@@ -163,11 +163,13 @@ hc_status hc_apply_carries(int D, hc_dtype dtype, const void* z, void* out, void
 /* Ordinary 1-D convolution out[m] = sum_i x[i] y[m - i], m < 2^(D+1) - 1, of two length-2^D
  * vectors: the carry-free (hypercube) convolution of their bit-axis embeddings followed by the
  * carries (PAPER.md 354-373).  plan: single-GPU plan of dimension D and the vectors' dtype.
- * z_work: 3^D elements (device workspace); out: 2^(D+1) - 1 elements (device, overwritten).
- * work: hc_carries_work_len(D) elements, or NULL for int64 plans with D >= 13 -- there the
- * carries are fused into the slab engine's pass 2 (every final z[k] is added into
- * out[sum_b k_b 2^b] with exact wrapping uint64 atomics), z_work only holds the pass-1 tiles
- * and z itself is never written.  fp64 and D < 13 run hc_convolve then hc_apply_carries.
+ * out: 2^(D+1) - 1 elements (device, overwritten).  For int64 plans with D >= 13 the carries
+ * are fused into the slab engine's pass 2 (every final z[k] is added into out[sum_b k_b 2^b]
+ * with exact wrapping uint64 atomics) and z is never formed; pass-1 tiles live in z_work
+ * (3^D elements) when it is given, else in a plan-owned ring of 4 slab buffers
+ * (4 x 3^min(D,14) elements, allocated on first use; ~4% slower at D = 20) -- work may be
+ * NULL.  Otherwise (fp64, D < 13) z_work (3^D elements, device) and work
+ * (hc_carries_work_len(D) elements) are required: hc_convolve, then hc_apply_carries.
  * Errors: HC_ERR_SHARD for a multi-rank plan; otherwise as hc_convolve. */
 hc_status hc_conv1d(hc_plan_t plan, const void* x, const void* y, void* z_work, void* out, void* work,
                     void* stream);

@@ -207,7 +207,7 @@ cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const Sla
   if (e != cudaSuccess) return e;
   const uint64_t items = (uint64_t)a.nslab * (upow3(M) + upow3(8) / (P2W * T8_P2CH));
   const unsigned grid = (unsigned)(items < (uint64_t)grid_max ? items : (uint64_t)grid_max);
-  e = cudaMemsetAsync(a.ctr, 0, sizeof(uint32_t) * (1 + (size_t)a.nslab), st);
+  e = cudaMemsetAsync(a.ctr, 0, sizeof(uint32_t) * (1 + 2 * (size_t)a.nslab), st);
   if (e != cudaSuccess) return e;
   {
     LaunchScope lp("prep", st);
@@ -258,10 +258,12 @@ cudaError_t launch_slabws_m(const T* x, const T* y, T* z, T* xu, T* yu, const Sl
 template <class T>
 cudaError_t launch_slab8(const T* x, const T* y, T* z, T* xu, T* yu, int M, const SlabArgs& a, cudaStream_t st) {
   if constexpr (std::is_same<T, uint64_t>::value) {
-    if (a.cout) {  // f1: carries fused into pass 2
-      switch (M) {
-        case 5: return launch_slab8_m<T, 5, 2>(x, y, z, xu, yu, a, st);
-        case 6: return launch_slab8_m<T, 6, 2>(x, y, z, xu, yu, a, st);
+    if (a.cout) {  // f1: carries fused into pass 2; tiles in z (2) or in the slab ring (3)
+      switch (M * 2 + (a.ring != nullptr)) {
+        case 10: return launch_slab8_m<T, 5, 2>(x, y, z, xu, yu, a, st);
+        case 11: return launch_slab8_m<T, 5, 3>(x, y, z, xu, yu, a, st);
+        case 12: return launch_slab8_m<T, 6, 2>(x, y, z, xu, yu, a, st);
+        case 13: return launch_slab8_m<T, 6, 3>(x, y, z, xu, yu, a, st);
         default: return cudaErrorInvalidValue;
       }
     }
@@ -368,6 +370,7 @@ struct hc_plan_s {
   Geometry g;
   std::vector<uint64_t> cuts;     // ngpu+1 unit (slab) boundaries (equal cost)
   uint32_t* ctr[3] = {nullptr, nullptr, nullptr};  // slab-engine counters (device, per stream slot)
+  void* ring = nullptr;  // hc_conv1d (fused carries): T8_RING slab buffers for pass-1 tiles
   void* xu = nullptr;             // two-level: middle-axes-evaluated input slices (prep kernel)
   void* yu = nullptr;
   std::mutex order_mu;
@@ -474,6 +477,7 @@ extern "C" hc_status hc_plan_destroy(hc_plan_t p) {
   for (auto& c : p->ctr) cudaFree(c);
   cudaFree(p->xu);
   cudaFree(p->yu);
+  cudaFree(p->ring);
   cudaFree(p->app_a);
   cudaFree(p->app_b);
   cudaFree(p->app_mx);
@@ -535,7 +539,7 @@ static const uint4* slab_order(hc_plan_t p, uint64_t u0, uint64_t u1) {
 
 // units [u0, u1) of the plan's geometry into z (z points at unit u0)
 static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, uint64_t u0, uint64_t u1,
-                           cudaStream_t st, int slot, unsigned long long* cout = nullptr) {
+                           cudaStream_t st, int slot, unsigned long long* cout = nullptr, void* ring = nullptr) {
   if (u1 <= u0) return HC_OK;
   const Geometry& g = p->g;
   cudaError_t e;
@@ -546,7 +550,7 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
     if (!order) return HC_ERR_CAPACITY;
     static const int dbg = getenv("HC_DEBUG_SKIP") ? atoi(getenv("HC_DEBUG_SKIP")) : 0;
     static const int lag = getenv("HC_SLAB_LAG") ? atoi(getenv("HC_SLAB_LAG")) : 1;
-    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg, (uint32_t)(lag < 1 ? 1 : lag), cout};
+    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg, (uint32_t)(lag < 1 ? 1 : lag), cout, ring};
 #ifdef HC_PHASE_PROF
     {
       unsigned long long zero[16] = {0};
@@ -922,17 +926,30 @@ extern "C" hc_status hc_apply_carries(int D, hc_dtype dtype, const void* z, void
 
 extern "C" hc_status hc_conv1d(hc_plan_t p, const void* x, const void* y, void* z_work, void* out, void* work,
                                void* stream) {
-  if (!p || !x || !y || !z_work || !out) return HC_ERR_NULL;
-  if (!aligned16(x) || !aligned16(y) || !aligned8(z_work) || !aligned8(out)) return HC_ERR_ALIGN;
+  if (!p || !x || !y || !out) return HC_ERR_NULL;
+  if (!aligned16(x) || !aligned16(y) || !aligned8(out)) return HC_ERR_ALIGN;
   if (p->ngpu != 1) return HC_ERR_SHARD;
   const int D = p->D;
   cudaStream_t st = (cudaStream_t)stream;
   if (p->dtype == HC_INT64 && p->g.two_level) {
     // the slab engine adds every final z[k] into out[val(k)] (uint64, exact in any order);
-    // z_work only holds the pass-1 tiles
+    // pass-1 tiles live in z_work when given (3^D), else in the plan's ring of slab buffers
     if (cudaMemsetAsync(out, 0, sizeof(uint64_t) * ((2ull << D) - 1), st) != cudaSuccess) return HC_ERR_CUDA;
-    return run_range(p, x, y, z_work, 0, p->g.nunits, st, 0, (unsigned long long*)out);
+    if (z_work) {
+      if (!aligned8(z_work)) return HC_ERR_ALIGN;
+      return run_range(p, x, y, z_work, 0, p->g.nunits, st, 0, (unsigned long long*)out, nullptr);
+    }
+    if (!p->ring) {
+      if (cudaMalloc(&p->ring, sizeof(uint64_t) * (size_t)p->g.unit * T8_RING) != cudaSuccess) {
+        cudaGetLastError();
+        p->ring = nullptr;
+        return HC_ERR_CAPACITY;
+      }
+    }
+    return run_range(p, x, y, nullptr, 0, p->g.nunits, st, 0, (unsigned long long*)out, p->ring);
   }
+  if (!z_work) return HC_ERR_NULL;
+  if (!aligned8(z_work)) return HC_ERR_ALIGN;
   if (D > 8 && !work) return HC_ERR_NULL;
   hc_status s = run_range(p, x, y, z_work, 0, p->g.nunits, st, 0);
   if (s != HC_OK) return s;

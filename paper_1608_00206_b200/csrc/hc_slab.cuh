@@ -448,6 +448,13 @@ __device__ __forceinline__ ItemDec decode_item(uint32_t q, uint32_t ns, uint32_t
 constexpr int T8_QN = HC_QN;  // claimed items held per CTA
 constexpr uint32_t T8_EXH = 0xffffffffu;
 constexpr int T8_DEFER = -2;  // s_sel: selection postponed past the item's closing barrier
+// EPI 3 (fused carries, ring): pass-1 tiles live in a ring of T8_RING slab buffers (slab position j
+// in slot j mod T8_RING) instead of z; a pass-1 item of position j >= T8_RING is ready once
+// every pass-2 item of position j - T8_RING (claimed earlier) has read its column
+#ifndef HC_RING
+#define HC_RING 4
+#endif
+constexpr uint32_t T8_RING = HC_RING;
 #ifndef HC_P2CH
 #define HC_P2CH 3
 #endif
@@ -548,7 +555,9 @@ struct __align__(16) Slot {
 };
 static_assert(T8_QN == 3, "the scheduler packs the slots' claim indices into one uint4");
 
-template <class T, int M, int EPI = 0>  // EPI 2: carries fused into pass 2 (f1, uint64 only)
+// EPI 2: carries fused into pass 2 (f1, uint64 only), tiles in place in z; EPI 3: the same
+// with the tiles in a ring of T8_RING slab buffers (no 3^D buffer)
+template <class T, int M, int EPI = 0>
 __global__ void __launch_bounds__(T8_NT, 2)
 slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__ z, SlabArgs args) {
   constexpr uint32_t N1 = (uint32_t)ipow3(M);
@@ -573,6 +582,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   const bool skip1 = args.debug_skip == 2, skip2 = args.debug_skip == 1;
   T* R = sm + T8Cfg<T>::ALIAS;
   uint32_t* done_ctr = args.ctr + 1;
+  uint32_t* p2_done = args.ctr + 1 + args.nslab;  // EPI 3: pass-2 items finished per position
 
   // T8_SCHED helpers -------------------------------------------------------------------
   auto decode = [&](uint32_t q, Slot& o) {
@@ -654,14 +664,14 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   // redone after the barrier, where signal() is safe.
   auto select_next = [&](bool may_wait) {
     PH_T0;
-    int sel, p2w;
-    uint32_t jw = 0;
+    int sel, wsl;        // wsl: the slot to wait for when nothing is ready
+    const uint32_t* wctr = nullptr;
+    uint32_t wneed = 0;
     for (int pass = 0;; ++pass) {
       const uint4 qm = s_qm, jm = s_jm;
-      const uint32_t rq[3] = {qm.x, qm.y, qm.z}, rj[3] = {jm.x, jm.y, jm.z};
-      int p2r = -1, p1 = -1;
+      const uint32_t rq[3] = {qm.x, qm.y, qm.z};
+      int p2r = -1, p1 = -1, p2w = -1;
       uint32_t q1 = T8_EXH, q2r = T8_EXH, q2w = T8_EXH;
-      p2w = -1;
 #pragma unroll
       for (int i = 0; i < T8_QN; ++i) {
         if (i == pslot || rq[i] == T8_EXH) continue;
@@ -670,26 +680,46 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
         } else if (skip2 || (((cmask >> i) & 1) && cv[i] >= N1)) {
           if (rq[i] < q2r) { q2r = rq[i]; p2r = i; }
         } else if (rq[i] < q2w) {
-          q2w = rq[i]; p2w = i; jw = rj[i];
+          q2w = rq[i]; p2w = i;
         }
       }
-      sel = p2r >= 0 ? p2r : (p1 >= 0 ? p1 : p2w);
+      // only the lowest pass-1 claim may run (the prefetcher loads slices in claim order);
+      // with the slab ring it may still have to wait for pass 2 of position j - T8_RING
+      bool p1_ready = p1 >= 0;
+      if constexpr (EPI == 3) {
+        if (p1 >= 0) {
+          const uint32_t j1 = p1 == 0 ? jm.x : (p1 == 1 ? jm.y : jm.z);
+          p1_ready = j1 < T8_RING || (((cmask >> p1) & 1) && cv[p1] >= N2);
+        }
+      }
+      sel = p2r >= 0 ? p2r : (p1_ready ? p1 : -1);
+      wsl = -1;
+      if (sel < 0) {  // wait for the lower claim of the blocked pass-1 item and pass-2 item
+        const bool w1 = p1 >= 0 && (p2w < 0 || q1 < q2w);
+        wsl = w1 ? p1 : p2w;
+        if (wsl >= 0) {
+          const uint32_t jw = wsl == 0 ? jm.x : (wsl == 1 ? jm.y : jm.z);
+          if (w1) { wctr = p2_done + (jw - T8_RING); wneed = N2; }
+          else { wctr = done_ctr + jw; wneed = N1; }
+        }
+        sel = wsl;
+      }
       // before waiting (or leaving), the pending claim must be visible: it may be the
       // pass-1 item everybody waits for
-      if ((sel < 0 || sel == p2w) && pslot >= 0 && pass == 0) {
+      if ((sel < 0 || wsl >= 0) && pslot >= 0 && pass == 0) {
         finish_pending();
         continue;
       }
       break;
     }
-    if (!may_wait && (sel < 0 || sel == p2w)) {
+    if (!may_wait && (sel < 0 || wsl >= 0)) {
       s_sel = T8_DEFER;
       return;
     }
-    if (sel >= 0 && sel == p2w) {  // nothing else to do: signal, then wait for the slab
+    if (wsl >= 0) {  // nothing else to do: signal, then wait for the dependency
       signal();
       pump();
-      while (ld_relaxed(done_ctr + jw) < N1) __nanosleep(64);
+      while (ld_relaxed(wctr) < wneed) __nanosleep(64);
     }
     if (sel < 0) signal();
     s_sel = sel;
@@ -719,11 +749,15 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
         if (i != sel && i != pslot && rq[i] != T8_EXH && !((qm.w >> i) & 1)) {
           cv[i] = ld_relaxed(done_ctr + rj[i]);  // non-blocking; compared at the next selection
           cmask |= 1u << i;
+        } else if (EPI == 3 && i != sel && i != pslot && rq[i] != T8_EXH && rj[i] >= T8_RING) {
+          cv[i] = ld_relaxed(p2_done + (rj[i] - T8_RING));  // pass-1 slot: its ring slot freed?
+          cmask |= 1u << i;
         }
       }
     }
     PH_MARK(0);
-    T* zs = z + (uint64_t)it.loc * SLAB;
+    T* zs = EPI == 3 ? reinterpret_cast<T*>(args.ring) + (uint64_t)(it.j % T8_RING) * SLAB
+                     : z + (uint64_t)it.loc * SLAB;
     if (it.p1) {
       if (skip1) {
         if (threadIdx.x == T8_SCHED) atomicAdd(done_ctr + it.j, 1u);
@@ -738,7 +772,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       // barrier, and go to L2 (.cg), where the producers' fenced stores already are
       if (threadIdx.x == T8_SCHED) pump();
       // three 9-column chunks per item (a third as many items to schedule), pipelined
-      if constexpr (EPI == 2) {
+      if constexpr (EPI >= 2) {
         // carry bins: val(k) = (tile digits) + 2^8 (middle digits) + 2^(8+M) (top digits)
         uint64_t vtop = 0;
         {
@@ -792,6 +826,12 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       select_next(false);
     }
     __syncthreads();  // the item's smem is free; s_sel is set
+    if constexpr (EPI == 3) {
+      // this pass-2 item has read its ring columns: every load's value was consumed before
+      // the barrier above, so the slot may be rewritten once the count is seen (no fence:
+      // a write-after-read hazard only)
+      if (threadIdx.x == T8_SCHED && !it.p1 && !skip2) atomicAdd(p2_done + it.j, 1u);
+    }
     if (*(volatile int*)&s_sel == T8_DEFER) {
       __syncthreads();  // everybody has seen T8_DEFER before it is overwritten
       if (threadIdx.x == T8_SCHED) select_next(true);

@@ -270,6 +270,7 @@ struct SlabArgs {
   int debug_skip;      // timing experiments only (HC_DEBUG_SKIP): 1 = no pass 2, 2 = no pass 1
   uint32_t lag;        // pass 2 of slab j is scheduled after pass 1 of slab j + lag (>= 1)
   unsigned long long* cout;  // slab8_kernel<uint64_t, M, 2>: carry bins (f1), else unused
+  void* ring;                // slab8_kernel<uint64_t, M, 2>: T8_RING slab buffers for pass-1 tiles
 };
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {

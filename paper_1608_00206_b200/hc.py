@@ -243,14 +243,16 @@ def conv1d(x, y, out=None, plan=None, stream=None, z_work=None):
     D = n.bit_length() - 1
     plan = plan or Plan(D, x.dtype)
     code = _dtype_code(x.dtype)
-    if z_work is None:
+    fused = code == HC_INT64 and D >= 13  # no z: plan-owned ring of slab buffers
+    if z_work is None and not fused:
         z_work = torch.empty(3 ** D, dtype=x.dtype, device=x.device)
     if out is None:
         out = torch.empty((2 << D) - 1, dtype=x.dtype, device=x.device)
-    fused = code == HC_INT64 and D >= 13
     wl = carries_work_len(D)
     work = None if (fused or wl == 0) else torch.empty(wl, dtype=x.dtype, device=x.device)
-    _ok(_lib.hc_conv1d(plan._h, _dev(x, n, code, "x"), _dev(y, n, code, "y"), _dev(z_work, 3 ** D, code, "z_work"),
+    # fused: z_work (if given) holds the pass-1 tiles in place; else the plan's slab ring
+    zp = _P(0) if z_work is None else _dev(z_work, 3 ** D, code, "z_work")
+    _ok(_lib.hc_conv1d(plan._h, _dev(x, n, code, "x"), _dev(y, n, code, "y"), zp,
                        _dev(out, (2 << D) - 1, code, "out"), _P(work.data_ptr()) if work is not None else _P(0),
                        _P(_stream_ptr(stream))), "hc_conv1d")
     return out

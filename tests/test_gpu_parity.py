@@ -537,10 +537,28 @@ def test_conv1d_fused_equals_convolve_then_carries(hc, D):
     x = hcgen.splitmix64(7700 + D, 0, 1 << D).view(np.int64)
     y = hcgen.splitmix64(7700 + D, 1, 1 << D).view(np.int64)
     xg, yg = _gpu(x), _gpu(y)
-    fused = hc.conv1d(xg, yg)
+    fused_ring = hc.conv1d(xg, yg)  # pass-1 tiles in the plan's ring of slab buffers
     z = torch.empty(3 ** D, dtype=torch.int64, device="cuda")
+    fused_inplace = hc.conv1d(xg, yg, z_work=z)  # tiles in place in z
     hc.Plan(D, "int64").convolve(xg, yg, z)
     ref = torch.empty((2 << D) - 1, dtype=torch.int64, device="cuda")
     hc.apply_carries(D, z, ref)
     torch.cuda.synchronize()
-    assert torch.equal(fused, ref)
+    assert torch.equal(fused_ring, ref)
+    assert torch.equal(fused_inplace, ref)
+
+
+def test_conv1d_d21_without_z(hc):
+    # int64 D = 21: the carry-free output would be 3^21 x 8 B = 84 GB; the fused path keeps only
+    # a ring of four slabs and the 2^22 - 1 carry bins.  Sampled m against sum_i x[i] y[m - i].
+    D = 21
+    x = hcgen.uniform_int(2121, 0, 1 << D, 0, (1 << 16) - 1)
+    y = hcgen.uniform_int(2121, 1, 1 << D, 0, (1 << 16) - 1)
+    free0 = torch.cuda.mem_get_info()[0]
+    out = hc.conv1d(_gpu(x), _gpu(y)).cpu().numpy()
+    assert torch.cuda.mem_get_info()[0] > free0 - (2 << 30)  # far less than z would take
+    rng = np.random.default_rng(21)
+    for m in list(rng.integers(0, (2 << D) - 1, 150)) + [0, 1, (1 << D) - 1, (2 << D) - 2]:
+        lo, hi = max(0, m - (1 << D) + 1), min(m, (1 << D) - 1)
+        i = np.arange(lo, hi + 1)
+        assert out[m] == int((x[i].astype(object) * y[m - i].astype(object)).sum())
