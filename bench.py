@@ -8,8 +8,16 @@ synthetic; hcgen).  With N > 1 GPUs (torchrun), the same D = 20 output is split 
 contiguous ranges (zero-communication split by top trits, PAPER.md 166-177): total work
 fixed -> "scaling": "strong"; time = max over ranks.
 
-Prints ONE JSON line on rank 0.  `--impl reference` times the oracle (Algorithm 1 in plain
-C, oracle/) on the host cores instead; under torchrun only rank 0 runs it.
+Prints ONE JSON line on rank 0: the contract keys, `roofline` (min-bytes HBM efficiency of
+the dominant kernel from in-library per-launch CUDA events, plus the 8.0 TB/s spec figure and
+ncu's DRAM GB/s), `co_roofline` (fp64 instructions of the two-level engine against the
+measured fp64 rate), `cpu_baseline` (the oracle on a bounded sample of output cells), `e2e`
+(hc_convolve_host with pinned host buffers), `gpu_launches` and `clocks`.  Workloads smaller
+than 2x L2 are timed step by step with an L2 flush in between.  `--workload` selects the
+other BASELINE configs and the SURVEY §8(f) application rows (f1 conv1d, f2 p-norm
+max-convolution, f4 differences); `--variant evalpoint[-peer]` the K5b split.
+`--impl reference` times the oracle (Algorithm 1 in plain C, oracle/) on the host cores
+instead; under torchrun only rank 0 runs it.
 """
 from __future__ import annotations
 
