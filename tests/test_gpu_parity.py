@@ -197,6 +197,19 @@ def test_errors(hc):
     with pytest.raises(hc.HCError) as ei:
         p.convolve(buf[1:17], buf[1:17], torch.empty(81, dtype=torch.int64, device="cuda"))
     assert ei.value.code == 4
+    # hc_conv1d: a multi-rank plan is rejected (HC_ERR_SHARD); the unfused route needs z_work
+    import ctypes
+    x13 = torch.zeros(1 << 13, dtype=torch.int64, device="cuda")
+    out13 = torch.empty((2 << 13) - 1, dtype=torch.int64, device="cuda")
+    with pytest.raises(hc.HCError) as ei:
+        hc.conv1d(x13, x13, out13, plan=hc.Plan(13, "int64", 2, 0))
+    assert ei.value.code == 9
+    xf = torch.zeros(1 << 9, dtype=torch.float64, device="cuda")
+    of = torch.empty((2 << 9) - 1, dtype=torch.float64, device="cuda")
+    pf = hc.Plan(9, "float64")
+    code = hc._lib.hc_conv1d(pf._h, ctypes.c_void_p(xf.data_ptr()), ctypes.c_void_p(xf.data_ptr()), None,
+                             ctypes.c_void_p(of.data_ptr()), None, None)
+    assert code == 3  # HC_ERR_NULL: fp64 needs the 3^D workspace
 
 
 @pytest.mark.parametrize("D,dtype", [(13, "float64"), (14, "int64"), (15, "float64")])
