@@ -575,3 +575,26 @@ def test_conv1d_d21_without_z(hc):
         lo, hi = max(0, m - (1 << D) + 1), min(m, (1 << D) - 1)
         i = np.arange(lo, hi + 1)
         assert out[m] == int((x[i].astype(object) * y[m - i].astype(object)).sum())
+
+
+def test_property_random_shapes(hc, orc):
+    # property check over random small problems: D, dtype, value range, batch size and shard
+    # split drawn from a seeded generator; every output against Algorithm 1
+    rng = np.random.default_rng(4242)
+    for trial in range(24):
+        D = int(rng.integers(1, 13))
+        dtype = "int64" if rng.random() < 0.6 else "float64"
+        if dtype == "int64":
+            lo = -int(rng.integers(0, 1 << 30))
+            x, y = hcgen.make_pair(D, "int64", "uniform", 9000 + trial, lo, int(rng.integers(1, 1 << 30)))
+        else:
+            x, y = hcgen.make_pair(D, "float64", "exp_norm", 9000 + trial)
+        want = orc.conv(x, y)
+        _assert_close(_run(hc, x, y).cpu().numpy(), want, x, y)
+        B = int(rng.integers(1, 5))
+        xb = np.stack([np.roll(x, b) for b in range(B)])
+        yb = np.stack([np.roll(y, 3 * b) for b in range(B)])
+        zb = torch.empty((B, 3 ** D), dtype=_gpu(x).dtype, device="cuda")
+        hc.convolve_batched(_gpu(xb), _gpu(yb), zb)
+        torch.cuda.synchronize()
+        _assert_close(zb.cpu().numpy(), orc.conv_batched(xb, yb), xb, yb)
