@@ -566,8 +566,8 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   __shared__ Slot s_slot[T8_QN];
-  __shared__ uint4 s_qm;  // {q of slots 0..2, mask of pass-1 slots}: one load for the selection
-  __shared__ uint4 s_jm;  // {j of slots 0..2, -}
+  __shared__ uint4 s_qm;  // {q of slots 0..2, -}: one load for the selection
+  __shared__ uint4 s_jm;  // {j of slots 0..2, byte i of .w = slot i is a pass-1 item}
   __shared__ int s_sel;
   __shared__ __align__(8) uint64_t raw_bar[T8_NRAW];
   __shared__ Prefetch pf;
@@ -629,16 +629,15 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   // Thread T8_SCHED's state.  The slots live in shared memory (few registers are free in the
   // pair loop); s_qm / s_jm mirror their claim indices, kinds and slabs so that the selection,
   // which the whole CTA waits for, is two shared loads and register logic.
-  auto set_meta = [&](int i, uint32_t q, bool p1, uint32_t j) {
-    uint32_t* qm = reinterpret_cast<uint32_t*>(&s_qm);
-    qm[i] = q;
-    qm[3] = p1 ? (qm[3] | 1u << i) : (qm[3] & ~(1u << i));
+  auto set_meta = [&](int i, uint32_t q, bool p1, uint32_t j) {  // plain stores, no read-modify-write
+    reinterpret_cast<uint32_t*>(&s_qm)[i] = q;
     reinterpret_cast<uint32_t*>(&s_jm)[i] = j;
+    reinterpret_cast<uint8_t*>(&s_jm.w)[i] = p1 ? 1 : 0;
   };
   if (threadIdx.x == T8_SCHED) {
     uint32_t c[T8_QN];
     for (int i = 0; i < T8_QN; ++i) c[i] = atomicAdd(args.ctr, 1u);
-    s_qm.w = 0;
+    s_jm.w = 0;
     for (int i = 0; i < T8_QN; ++i) {
       decode(c[i], s_slot[i]);
       set_meta(i, s_slot[i].q, s_slot[i].q != T8_EXH && s_slot[i].p1, s_slot[i].j);
@@ -675,7 +674,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
 #pragma unroll
       for (int i = 0; i < T8_QN; ++i) {
         if (i == pslot || rq[i] == T8_EXH) continue;
-        if ((qm.w >> i) & 1) {
+        if ((jm.w >> (8 * i)) & 1) {
           if (rq[i] < q1) { q1 = rq[i]; p1 = i; }
         } else if (skip2 || (((cmask >> i) & 1) && cv[i] >= N1)) {
           if (rq[i] < q2r) { q2r = rq[i]; p2r = i; }
@@ -746,7 +745,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       const uint32_t rq[3] = {qm.x, qm.y, qm.z}, rj[3] = {jm.x, jm.y, jm.z};
 #pragma unroll
       for (int i = 0; i < T8_QN; ++i) {
-        if (i != sel && i != pslot && rq[i] != T8_EXH && !((qm.w >> i) & 1)) {
+        if (i != sel && i != pslot && rq[i] != T8_EXH && !((jm.w >> (8 * i)) & 1)) {
           cv[i] = ld_relaxed(done_ctr + rj[i]);  // non-blocking; compared at the next selection
           cmask |= 1u << i;
         } else if (EPI == 3 && i != sel && i != pslot && rq[i] != T8_EXH && rj[i] >= T8_RING) {
