@@ -329,9 +329,10 @@ __device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, Raw
     for (int e = 0; e < 27; ++e) S[a * 729 + e * 27 + c] = v[e];
   }
   __syncthreads();
-  if (unit) {  // columns (k_B, k_C), three rounds of 243: interpolate the A axes, store
+  // columns (k_B, k_C), three rounds of 243: interpolate the A axes, store
 #pragma unroll 1
-    for (int r = 0; r < 3; ++r) {
+  for (int r = 0; r < 3; ++r) {
+    if (unit) {
       const int col = r * 243 + tid;
       T v[9];
 #pragma unroll
@@ -342,6 +343,12 @@ __device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, Raw
         if constexpr (FINAL) st_cs(zt + e * 729 + col, v[e]);
         else st_hint(zt + e * 729 + col, v[e], pol_out);
       }
+    }
+    // single level: keeping the CTA's rounds of final (streaming) stores in step measured
+    // faster (batched D = 8: 1.17 vs 1.185 ms); the slab engine's tiles go to L2 and do not
+    // gain (27.68 vs 27.55 ms at D = 20)
+    if constexpr (FINAL) {
+      if (r < 2) __syncthreads();
     }
   }
 }
