@@ -175,6 +175,18 @@ def test_host_entry_point(hc, orc):
     zd = _run(hc, x, y).cpu()
     assert torch.equal(zh, zd)
     _assert_close(zh.numpy(), orc.conv(x, y), x, y)
+    # a shard of a 3-way split through the host entry point (chunked device output and
+    # overlapped copies), int64 at D = 16 and D = 8 (single-level), = the device path
+    for D, n, r in ((16, 3, 1), (8, 1, 0), (10, 3, 2)):
+        x, y = hcgen.make_pair(D, "int64", "uniform", 78 + D, -1000, 1000)
+        p = hc.Plan(D, "int64", n, r)
+        b, e = p.shard_info()
+        zh = torch.empty(e - b, dtype=torch.int64).pin_memory()
+        p.convolve_host(torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory(), zh)
+        zd = torch.empty(e - b, dtype=torch.int64, device="cuda")
+        p.convolve_sharded(_gpu(x), _gpu(y), zd)
+        torch.cuda.synchronize()
+        assert torch.equal(zh, zd.cpu())
 
 
 def test_commutativity_int64(hc):
