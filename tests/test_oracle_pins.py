@@ -265,3 +265,18 @@ def test_ternary_map(orc):
     # T(i) = sum_b bit_b(i) 3^b (PAPER.md 109-112)
     for i in [0, 1, 2, 3, 7, 5, (1 << 22) - 1]:
         assert orc.ternary_of_binary(i) == sum(((i >> b) & 1) * 3 ** b for b in range(23))
+
+
+def test_spec_worked_values_and_zero(orc):
+    # SPEC.md 183-184 worked values (golden file, with citations) and the zero annihilator
+    # (SPEC.md 138): x * 0 = 0 for any x
+    g = _read_golden("spec_examples.txt")
+    for n in ("1", "2"):
+        x = np.array(g["x" + n], dtype=np.int64)
+        y = np.array(g["y" + n], dtype=np.int64)
+        assert orc.conv(x, y).tolist() == g["z" + n]
+        assert orc.conv(y, x).tolist() == g["z" + n]
+    rng = np.random.default_rng(138)
+    for D in (1, 3, 6):
+        x = rng.integers(-1000, 1000, 1 << D).astype(np.int64)
+        assert not orc.conv(x, np.zeros_like(x)).any()
