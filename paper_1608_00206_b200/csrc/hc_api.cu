@@ -18,7 +18,6 @@
 #include "hc_common.cuh"
 #include "hc_tile.cuh"
 #include "hc_slab.cuh"
-#include "hc_ws.cuh"
 
 using namespace hc;
 
@@ -161,30 +160,6 @@ cudaError_t t8_grid(K kern, int& grid_max) {
 template <class T>
 cudaError_t launch_tile8(const T* x, const T* y, T* z, int D, uint64_t slab0, uint64_t nslab, uint64_t nitems,
                          cudaStream_t st) {
-  // HC_TILE_WS=1: warp-specialised variant (tilews_kernel); measured slower than the fork-join
-  // tile8_kernel on B200 (batched D=8: 1.44 vs 1.17 ms), kept for experiments
-  static const int ws = getenv("HC_TILE_WS") ? atoi(getenv("HC_TILE_WS")) : 0;
-  if (ws) {
-    auto kern = tilews_kernel<T>;
-    static int gm_cache[kMaxDev] = {};
-    int gm_scratch = 0;
-    int& grid_max = dev_slot(gm_cache, gm_scratch);
-    if (!grid_max) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TWSCfg::SMEM);
-      if (e != cudaSuccess) return e;
-      int occ = 0, dev = 0, sms = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WS_NT, TWSCfg::SMEM);
-      if (e != cudaSuccess) return e;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (occ < 1) return cudaErrorInvalidConfiguration;
-      grid_max = occ * sms;
-    }
-    const unsigned grid = (unsigned)(nitems < (uint64_t)grid_max ? nitems : (uint64_t)grid_max);
-    LaunchScope ls("tile", st);
-    kern<<<grid, WS_NT, TWSCfg::SMEM, st>>>(x, y, z, D, slab0, nslab, nitems);
-    return cudaGetLastError();
-  }
   auto kern = tile8_kernel<T>;
   static int gm_cache[kMaxDev] = {};
   int gm_scratch = 0;
@@ -197,8 +172,17 @@ cudaError_t launch_tile8(const T* x, const T* y, T* z, int D, uint64_t slab0, ui
   return cudaGetLastError();
 }
 
+template <class T, int M>
+cudaError_t launch_prep(const T* x, const T* y, T* xu, T* yu, int k, cudaStream_t st) {
+  LaunchScope lp("prep", st);
+  dim3 pg((unsigned)upow3(M), 1u << k, 2);
+  prep_kernel<T, M><<<pg, 256, 0, st>>>(x, y, xu, yu);
+  return cudaGetLastError();
+}
+
 template <class T, int M, int EPI = 0>
-cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st) {
+cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st,
+                           bool prep) {
   auto kern = slab8_kernel<T, M, EPI>;
   static int gm_cache[kMaxDev] = {};
   int gm_scratch = 0;
@@ -209,11 +193,8 @@ cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const Sla
   const unsigned grid = (unsigned)(items < (uint64_t)grid_max ? items : (uint64_t)grid_max);
   e = cudaMemsetAsync(a.ctr, 0, sizeof(uint32_t) * (1 + 2 * (size_t)a.nslab), st);
   if (e != cudaSuccess) return e;
-  {
-    LaunchScope lp("prep", st);
-    dim3 pg((unsigned)upow3(M), 1u << a.k, 2);
-    prep_kernel<T, M><<<pg, 256, 0, st>>>(x, y, xu, yu);
-    e = cudaGetLastError();
+  if (prep) {
+    e = launch_prep<T, M>(x, y, xu, yu, a.k, st);
     if (e != cudaSuccess) return e;
   }
   LaunchScope ls("slab", st);
@@ -221,64 +202,23 @@ cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const Sla
   return cudaGetLastError();
 }
 
-// warp-specialised variant (hc_ws.cuh): one CTA per SM
-template <class T, int M>
-cudaError_t launch_slabws_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st) {
-  auto kern = slabws_kernel<T, M>;
-  static int gm_cache[kMaxDev] = {};
-  int gm_scratch = 0;
-  int& grid_max = dev_slot(gm_cache, gm_scratch);
-  if (!grid_max) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WSCfg<T, M>::SMEM);
-    if (e != cudaSuccess) return e;
-    int occ = 0, dev = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WS_NT, WSCfg<T, M>::SMEM);
-    if (e != cudaSuccess) return e;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (occ < 1) return cudaErrorInvalidConfiguration;
-    grid_max = occ * sms;
-  }
-  const uint64_t tiles = (uint64_t)a.nslab * upow3(M);
-  const unsigned grid = (unsigned)(tiles < (uint64_t)grid_max ? tiles : (uint64_t)grid_max);
-  cudaError_t e = cudaMemsetAsync(a.ctr, 0, sizeof(uint32_t) * (2 + 2 * (size_t)a.nslab), st);
-  if (e != cudaSuccess) return e;
-  {
-    LaunchScope lp("prep", st);
-    dim3 pg((unsigned)upow3(M), 1u << a.k, 2);
-    prep_kernel<T, M><<<pg, 256, 0, st>>>(x, y, xu, yu);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  LaunchScope ls("slab", st);
-  kern<<<grid, WS_NT, WSCfg<T, M>::SMEM, st>>>(xu, yu, z, a);
-  return cudaGetLastError();
-}
-
 template <class T>
-cudaError_t launch_slab8(const T* x, const T* y, T* z, T* xu, T* yu, int M, const SlabArgs& a, cudaStream_t st) {
+cudaError_t launch_slab8(const T* x, const T* y, T* z, T* xu, T* yu, int M, const SlabArgs& a, cudaStream_t st,
+                         bool prep) {
   if constexpr (std::is_same<T, uint64_t>::value) {
     if (a.cout) {  // f1: carries fused into pass 2; tiles in z (2) or in the slab ring (3)
       switch (M * 2 + (a.ring != nullptr)) {
-        case 10: return launch_slab8_m<T, 5, 2>(x, y, z, xu, yu, a, st);
-        case 11: return launch_slab8_m<T, 5, 3>(x, y, z, xu, yu, a, st);
-        case 12: return launch_slab8_m<T, 6, 2>(x, y, z, xu, yu, a, st);
-        case 13: return launch_slab8_m<T, 6, 3>(x, y, z, xu, yu, a, st);
+        case 10: return launch_slab8_m<T, 5, 2>(x, y, z, xu, yu, a, st, prep);
+        case 11: return launch_slab8_m<T, 5, 3>(x, y, z, xu, yu, a, st, prep);
+        case 12: return launch_slab8_m<T, 6, 2>(x, y, z, xu, yu, a, st, prep);
+        case 13: return launch_slab8_m<T, 6, 3>(x, y, z, xu, yu, a, st, prep);
         default: return cudaErrorInvalidValue;
       }
     }
   }
-  static const int ws = getenv("HC_SLAB_WS") ? atoi(getenv("HC_SLAB_WS")) : 0;
-  if (ws) {
-    switch (M) {
-      case 5: return launch_slabws_m<T, 5>(x, y, z, xu, yu, a, st);
-      case 6: return launch_slabws_m<T, 6>(x, y, z, xu, yu, a, st);
-      default: return cudaErrorInvalidValue;
-    }
-  }
   switch (M) {
-    case 5: return launch_slab8_m<T, 5>(x, y, z, xu, yu, a, st);
-    case 6: return launch_slab8_m<T, 6>(x, y, z, xu, yu, a, st);
+    case 5: return launch_slab8_m<T, 5>(x, y, z, xu, yu, a, st, prep);
+    case 6: return launch_slab8_m<T, 6>(x, y, z, xu, yu, a, st, prep);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -297,14 +237,13 @@ cudaError_t launch_tile_cfg(const T* x, const T* y, T* z, int D, uint64_t slab0,
     if (e != cudaSuccess) return e;
     attr_set = 1;
   }
+  // items [off, off + n) per launch (gridDim.x <= 2^31 - 1): the kernel gets the item offset,
+  // so batch and slab indices stay exact across chunks
   const uint64_t maxgrid = 0x7fffffffull;
   for (uint64_t off = 0; off < nitems; off += maxgrid) {
     const uint64_t n = nitems - off < maxgrid ? nitems - off : maxgrid;
-    // items [off, off+n): shift z and the slab origin; batches only appear with nslab = 3^k
     LaunchScope ls("tile", st);
-    // when off > 0 the batch/slab split must be recomputed; offsets are multiples of nslab
-    // only for batched calls, so restrict chunking to whole batches or single-batch ranges
-    kern<<<(unsigned)n, Cfg::NT, Cfg::SMEM, st>>>(x, y, z + off * (uint64_t)Cfg::NOUT, D, slab0 + off, nslab);
+    kern<<<(unsigned)n, Cfg::NT, Cfg::SMEM, st>>>(x, y, z, D, slab0, nslab, off);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -429,6 +368,8 @@ extern "C" hc_status hc_shard_range(int D, int ngpu, int rank, uint64_t* zb, uin
   return HC_OK;
 }
 
+static const uint4* slab_order(hc_plan_t p, uint64_t u0, uint64_t u1);
+
 extern "C" hc_status hc_plan_create(hc_plan_t* out, int D, hc_dtype dtype, int ngpu, int rank) {
   if (!out) return HC_ERR_NULL;
   *out = nullptr;
@@ -460,6 +401,12 @@ extern "C" hc_status hc_plan_create(hc_plan_t* out, int D, hc_dtype dtype, int n
     const size_t bytes = sizeof(double) * (size_t)(1ull << g.k) * upow3(g.M) * 256;
     if (cudaMalloc(&p->xu, bytes) != cudaSuccess || cudaMalloc(&p->yu, bytes) != cudaSuccess) {
       cudaGetLastError();
+      hc_plan_destroy(p);
+      return HC_ERR_CAPACITY;
+    }
+    // the slab processing order of the plan's own range is uploaded here, so hc_convolve /
+    // hc_convolve_sharded do no synchronous work (stream-ordered, graph-capturable)
+    if (!slab_order(p, p->cuts[rank], p->cuts[rank + 1])) {
       hc_plan_destroy(p);
       return HC_ERR_CAPACITY;
     }
@@ -498,7 +445,9 @@ extern "C" hc_status hc_shard_info(hc_plan_t p, int rank, uint64_t* zb, uint64_t
 
 // Processing order of the slabs [u0, u1) for the slab engine: sorted by the number of
 // direct-split pairs 2^{#1(t_T)} so that consecutive slabs cost the same and a pass-2 item
-// rarely waits for a slow pass-1 item of its slab.  Cached per range on the plan.
+// rarely waits for a slow pass-1 item of its slab.  Cached per range on the plan; the plan's
+// own range is built at plan creation, other ranges (the host entry point's chunks) on their
+// first use inside hc_convolve_host, which synchronises anyway.
 static const uint4* slab_order(hc_plan_t p, uint64_t u0, uint64_t u1) {
   std::lock_guard<std::mutex> lk(p->order_mu);
   auto key = std::make_pair(u0, u1);
@@ -539,7 +488,8 @@ static const uint4* slab_order(hc_plan_t p, uint64_t u0, uint64_t u1) {
 
 // units [u0, u1) of the plan's geometry into z (z points at unit u0)
 static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, uint64_t u0, uint64_t u1,
-                           cudaStream_t st, int slot, unsigned long long* cout = nullptr, void* ring = nullptr) {
+                           cudaStream_t st, int slot, unsigned long long* cout = nullptr, void* ring = nullptr,
+                           bool prep = true) {
   if (u1 <= u0) return HC_OK;
   const Geometry& g = p->g;
   cudaError_t e;
@@ -550,7 +500,11 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
     if (!order) return HC_ERR_CAPACITY;
     static const int dbg = getenv("HC_DEBUG_SKIP") ? atoi(getenv("HC_DEBUG_SKIP")) : 0;
     static const int lag = getenv("HC_SLAB_LAG") ? atoi(getenv("HC_SLAB_LAG")) : 1;
-    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg, (uint32_t)(lag < 1 ? 1 : lag), cout, ring};
+    // lag >= 1; with the slab ring (fused carries) a pass-1 item of position j waits for the
+    // pass-2 items of j - T8_RING, which must be claimed earlier: lag <= T8_RING - 1
+    uint32_t lg = (uint32_t)(lag < 1 ? 1 : lag);
+    if (ring && lg > T8_RING - 1) lg = T8_RING - 1;
+    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg, lg, cout, ring};
 #ifdef HC_PHASE_PROF
     {
       unsigned long long zero[16] = {0};
@@ -559,10 +513,10 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
 #endif
     if (p->dtype == HC_INT64)
       e = launch_slab8<uint64_t>((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)z, (uint64_t*)p->xu,
-                                 (uint64_t*)p->yu, g.M, a, st);
+                                 (uint64_t*)p->yu, g.M, a, st, prep);
     else
       e = launch_slab8<double>((const double*)x, (const double*)y, (double*)z, (double*)p->xu, (double*)p->yu,
-                               g.M, a, st);
+                               g.M, a, st, prep);
 #ifdef HC_PHASE_PROF
     {
       unsigned long long h[16];
@@ -570,16 +524,25 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
       cudaStreamSynchronize(st);
       double tot = 0;
       for (int i : {0, 1, 4, 5, 6}) tot += (double)h[i];
-      if (getenv("HC_SLAB_WS") && atoi(getenv("HC_SLAB_WS")))
-        fprintf(stderr, "ws phase (Mclk, CTA sum): compute: throttle %.0f pairloop %.0f S-wait %.0f handoff %.0f | "
-                "epilogue: tiles %.0f p2 %.0f idle %.0f\n", h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6,
-                h[4] / 1e6, h[5] / 1e6, h[6] / 1e6);
-      else
       fprintf(stderr, "phase(Mclk/CTA-sum): select+wait %.0f pairloop %.0f inv+store %.0f p2 %.0f end %.0f "
               "(tot %.0f) | F1 mbar wait %.0f | t224 select %.0f end %.0f\n", h[0] / 1e6, h[1] / 1e6, h[6] / 1e6,
               h[4] / 1e6, h[5] / 1e6, tot / 1e6, h[7] / 1e6, h[2] / 1e6, h[3] / 1e6);
     }
 #endif
+  }
+  return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
+}
+
+// middle-axes tables of the two-level engine for inputs x, y (prep_kernel) on stream st
+static hc_status run_prep(hc_plan_t p, const void* x, const void* y, cudaStream_t st) {
+  const Geometry& g = p->g;
+  cudaError_t e = cudaErrorInvalidValue;
+  if (p->dtype == HC_INT64) {
+    if (g.M == 5) e = launch_prep<uint64_t, 5>((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)p->xu, (uint64_t*)p->yu, g.k, st);
+    if (g.M == 6) e = launch_prep<uint64_t, 6>((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)p->xu, (uint64_t*)p->yu, g.k, st);
+  } else {
+    if (g.M == 5) e = launch_prep<double, 5>((const double*)x, (const double*)y, (double*)p->xu, (double*)p->yu, g.k, st);
+    if (g.M == 6) e = launch_prep<double, 6>((const double*)x, (const double*)y, (double*)p->xu, (double*)p->yu, g.k, st);
   }
   return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
 }
@@ -607,9 +570,52 @@ extern "C" hc_status hc_convolve_batched(int B, int D, hc_dtype dtype, const voi
   const int L = D < kTileL ? D : kTileL;
   const uint64_t nslab = upow3(D - L);
   const uint64_t nitems = (uint64_t)B * nslab;
-  if (nitems > 0x7fffffffull) return HC_ERR_INVALID_DIM;
   cudaError_t e = launch_any(dtype, x, y, z, D, 0, nslab, nitems, (cudaStream_t)stream);
   return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
+}
+
+static void host_ws_free(hc_plan_t p) {
+  cudaFree(p->dx);
+  cudaFree(p->dy);
+  cudaFree(p->dz[0]);
+  cudaFree(p->dz[1]);
+  p->dx = p->dy = p->dz[0] = p->dz[1] = nullptr;
+  for (auto& s : p->hs) {
+    if (s) cudaStreamDestroy(s);
+    s = nullptr;
+  }
+  p->chunk_units = 0;
+}
+
+// host-entry workspace: inputs, two chunk buffers of ~1 GiB of output, two streams; on any
+// failure everything is released (no half-initialised state survives to the next call)
+static hc_status host_ws_alloc(hc_plan_t p) {
+  if (p->dx && p->dy && p->dz[0] && p->dz[1] && p->hs[0] && p->hs[1]) return HC_OK;
+  host_ws_free(p);
+  const size_t esz = 8;
+  const uint64_t nin = 1ull << p->D, tile = p->g.unit;
+  const uint64_t s0 = p->cuts[p->rank], s1 = p->cuts[p->rank + 1];
+  uint64_t cs = ((1ull << 30) / esz) / tile;
+  if (cs > s1 - s0) cs = s1 - s0;
+  if (cs < 1) cs = 1;
+  bool ok = cudaMalloc(&p->dx, nin * esz) == cudaSuccess && cudaMalloc(&p->dy, nin * esz) == cudaSuccess &&
+            cudaMalloc(&p->dz[0], cs * tile * esz) == cudaSuccess &&
+            cudaMalloc(&p->dz[1], cs * tile * esz) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    host_ws_free(p);
+    return HC_ERR_CAPACITY;
+  }
+  for (auto& s : p->hs) {
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaGetLastError();
+      s = nullptr;
+      host_ws_free(p);
+      return HC_ERR_CUDA;
+    }
+  }
+  p->chunk_units = cs;
+  return HC_OK;
 }
 
 extern "C" hc_status hc_convolve_host(hc_plan_t p, const void* xh, const void* yh, void* zh, void* stream) {
@@ -619,44 +625,39 @@ extern "C" hc_status hc_convolve_host(hc_plan_t p, const void* xh, const void* y
   const uint64_t tile = p->g.unit;
   const uint64_t s0 = p->cuts[p->rank], s1 = p->cuts[p->rank + 1];
   cudaStream_t st = (cudaStream_t)stream;
-  if (!p->dx) {
-    if (cudaMalloc(&p->dx, nin * esz) != cudaSuccess || cudaMalloc(&p->dy, nin * esz) != cudaSuccess) {
-      cudaGetLastError();
-      return HC_ERR_CAPACITY;
-    }
-    // chunks of ~1 GiB of output, double-buffered so D2H of chunk c overlaps chunk c+1
-    uint64_t cs = ((1ull << 30) / esz) / tile;
-    if (cs < 1) cs = 1;
-    if (cs > s1 - s0) cs = s1 - s0;
-    if (cs < 1) cs = 1;
-    p->chunk_units = cs;
-    for (int i = 0; i < 2; ++i) {
-      if (cudaMalloc(&p->dz[i], cs * tile * esz) != cudaSuccess) {
-        cudaGetLastError();
-        return HC_ERR_CAPACITY;
-      }
-      if (cudaStreamCreateWithFlags(&p->hs[i], cudaStreamNonBlocking) != cudaSuccess) return HC_ERR_CUDA;
-    }
-  }
+  hc_status hs = host_ws_alloc(p);
+  if (hs != HC_OK) return hs;
+  // every chunk's slab order exists before the first launch (built once per range)
+  if (p->g.two_level)
+    for (uint64_t c = s0; c < s1; c += p->chunk_units)
+      if (!slab_order(p, c, c + p->chunk_units < s1 ? c + p->chunk_units : s1)) return HC_ERR_CAPACITY;
   if (cudaMemcpyAsync(p->dx, xh, nin * esz, cudaMemcpyHostToDevice, st) != cudaSuccess) return HC_ERR_CUDA;
   if (cudaMemcpyAsync(p->dy, yh, nin * esz, cudaMemcpyHostToDevice, st) != cudaSuccess) return HC_ERR_CUDA;
-  cudaEvent_t ready;
-  cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
-  cudaEventRecord(ready, st);
-  int i = 0;
-  for (uint64_t c = s0; c < s1; c += p->chunk_units, i ^= 1) {
-    const uint64_t ce = c + p->chunk_units < s1 ? c + p->chunk_units : s1;
-    cudaStream_t hs = p->hs[i];
-    cudaStreamWaitEvent(hs, ready, 0);
-    hc_status r = run_range(p, p->dx, p->dy, p->dz[i], c, ce, hs, 1 + i);
+  // the middle-axes tables of the two-level engine depend only on x, y: built once on the
+  // input stream, before the chunks (which then skip it)
+  if (p->g.two_level) {
+    hc_status r = run_prep(p, p->dx, p->dy, st);
     if (r != HC_OK) return r;
+  }
+  cudaEvent_t ready;
+  if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess) return HC_ERR_CUDA;
+  hc_status r = HC_OK;
+  if (cudaEventRecord(ready, st) != cudaSuccess) r = HC_ERR_CUDA;
+  int i = 0;
+  for (uint64_t c = s0; c < s1 && r == HC_OK; c += p->chunk_units, i ^= 1) {
+    const uint64_t ce = c + p->chunk_units < s1 ? c + p->chunk_units : s1;
+    cudaStream_t hs2 = p->hs[i];
+    if (cudaStreamWaitEvent(hs2, ready, 0) != cudaSuccess) { r = HC_ERR_CUDA; break; }
+    r = run_range(p, p->dx, p->dy, p->dz[i], c, ce, hs2, 1 + i, nullptr, nullptr, /*prep=*/false);
+    if (r != HC_OK) break;
     if (cudaMemcpyAsync((char*)zh + (c - s0) * tile * esz, p->dz[i], (ce - c) * tile * esz,
-                        cudaMemcpyDeviceToHost, hs) != cudaSuccess)
-      return HC_ERR_CUDA;
+                        cudaMemcpyDeviceToHost, hs2) != cudaSuccess)
+      r = HC_ERR_CUDA;
   }
   cudaError_t e1 = cudaStreamSynchronize(p->hs[0]);
   cudaError_t e2 = cudaStreamSynchronize(p->hs[1]);
   cudaEventDestroy(ready);
+  if (r != HC_OK) return r;
   return (e1 == cudaSuccess && e2 == cudaSuccess) ? HC_OK : HC_ERR_CUDA;
 }
 

@@ -728,6 +728,10 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       while (ld_relaxed(wctr) < wneed) __nanosleep(64);
     }
     if (sel < 0) signal();
+    // a pass-2 item's slab was seen complete through a relaxed counter load (above, or
+    // snapshotted in cv[] one item earlier): the fence makes that observation an acquire, and
+    // the CTA barrier after the selection orders every thread's column loads after it
+    if (sel >= 0 && !((s_jm.w >> (8 * sel)) & 1)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
     s_sel = sel;
     PH_T1(2);
   };

@@ -233,16 +233,16 @@ __device__ __forceinline__ void p1_tile(const T* __restrict__ x, const T* __rest
   }
 }
 
-// Single-level tile kernel (all D <= 12, and batched): work item w covers batch
+// Single-level tile kernel (D <= 7, and batched D <= 7): work item w covers batch
 // b = w / nslab, top index t_T = slab0 + w % nslab, and writes z[w * 3^L ...].
 template <class T, int C, int B, int A>
 __global__ void __launch_bounds__(TileCfg<T, C, B, A>::NT)
 tile_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z, int D,
-            uint64_t slab0, uint64_t nslab) {
+            uint64_t slab0, uint64_t nslab, uint64_t w0) {
   using Cfg = TileCfg<T, C, B, A>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  const uint64_t w = blockIdx.x;
+  const uint64_t w = w0 + blockIdx.x;  // item index (launches of > 2^31 - 1 items are chunked)
   const uint64_t b = w / nslab;
   const uint64_t tT = slab0 + (w - b * nslab);
   p1_tile<T, C, B, A, true>(x + (b << D), y + (b << D), z + w * (uint64_t)Cfg::NOUT, D - Cfg::L, 0, tT, 0u, sm);

@@ -241,8 +241,15 @@ def conv1d(x, y, out=None, plan=None, stream=None, z_work=None):
     import torch
     n = x.numel()
     D = n.bit_length() - 1
-    plan = plan or Plan(D, x.dtype)
+    if n < 2 or (1 << D) != n:
+        raise ValueError(f"conv1d: x must have length 2^D with D >= 1, got {n}")
+    if y.numel() != n:
+        raise ValueError(f"conv1d: y has {y.numel()} elements, x has {n}")
     code = _dtype_code(x.dtype)
+    plan = plan or Plan(D, x.dtype)
+    if plan.D != D or plan.dtype_code != code:
+        raise ValueError(f"conv1d: plan is (D={plan.D}, dtype code {plan.dtype_code}), inputs are "
+                         f"(D={D}, dtype code {code})")
     fused = code == HC_INT64 and D >= 13  # no z: plan-owned ring of slab buffers
     if z_work is None and not fused:
         z_work = torch.empty(3 ** D, dtype=x.dtype, device=x.device)

@@ -463,10 +463,30 @@ def test_scheduler_race_stress(hc, orc):
             assert np.array_equal(torch.cat(parts).cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("var", ["HC_SLAB_WS", "HC_TILE_WS"])
-def test_warp_specialised_variants(var):
-    # the opt-in warp-specialised kernels (hc_ws.cuh) are selected by environment variables
-    # read once per process: run them in a child process against the oracle
+def test_slab_ring_lag_clamped():
+    # HC_SLAB_LAG beyond the fused-carry slab ring (4 buffers) is clamped to 3: the 1-D
+    # convolution through the ring still equals numpy's (no deadlock, no overwritten slot)
+    import subprocess
+    import sys
+    import os
+    code = (
+        "import sys; sys.path.insert(0, '.'); import numpy as np, torch, hcgen;"
+        "import paper_1608_00206_b200.hc as hc\n"
+        "for D in (13, 16):\n"
+        "    x, y = hcgen.make_pair(D, 'int64', 'uniform', 7300 + D, -999, 999)\n"
+        "    out = hc.conv1d(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())\n"
+        "    torch.cuda.synchronize(); assert np.array_equal(out.cpu().numpy(), np.convolve(x, y)), D\n"
+        "print('ok')\n")
+    env = dict(os.environ, HC_SLAB_LAG="4")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("env", [{"HC_SLAB_LAG": "2"}])
+def test_engine_variants_by_env(env):
+    # engine knobs are environment variables read once per process: run them in a child
+    # process against the oracle
     import subprocess
     import sys
     import os
@@ -483,7 +503,7 @@ def test_warp_specialised_variants(var):
         "hc.convolve_batched(torch.from_numpy(xb).cuda(), torch.from_numpy(yb).cuda(), zb)\n"
         "torch.cuda.synchronize(); assert np.array_equal(zb.cpu().numpy(), oracle.conv_batched(xb, yb))\n"
         "print('ok')\n")
-    env = dict(os.environ, **{var: "1", "HC_SLAB_LAG": "2"})
+    env = dict(os.environ, **env)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -280,3 +280,89 @@ def test_spec_worked_values_and_zero(orc):
     for D in (1, 3, 6):
         x = rng.integers(-1000, 1000, 1 << D).astype(np.int64)
         assert not orc.conv(x, np.zeros_like(x)).any()
+
+
+# ---------------------------------------------------------------------------------------
+# Direct pins for the two oracle entry points the GPU tests use as checkers beyond the
+# full-output gather (orc_conv_batched_f64, orc_conv_cells_i64).  Both are pinned against
+# the independent multi-index brute force (PAPER.md 40-60), the all-ones closed form
+# (PAPER.md 168-170: z[k] = 2^{#trits(k)=1}) and separable inputs (axis peeling, PAPER.md
+# 153-164), never against the oracle's own full-output function.
+def _ones_closed_form(D):
+    ones = np.zeros(1, dtype=np.int64)
+    for _ in range(D):
+        ones = np.concatenate([ones, ones + 1, ones])
+    return (1 << ones).astype(np.int64)
+
+
+def _separable_closed_form(fx, fy):
+    D = fx.shape[0]
+    want = np.ones(1, dtype=np.int64)
+    for b in range(D):
+        c = [fx[b, 0] * fy[b, 0], fx[b, 0] * fy[b, 1] + fx[b, 1] * fy[b, 0], fx[b, 1] * fy[b, 1]]
+        want = np.concatenate([want * c[0], want * c[1], want * c[2]])
+    return want
+
+
+@pytest.mark.parametrize("D", [1, 2, 3, 4])
+def test_batched_f64_bruteforce_and_stride(orc, D):
+    # every batch row against the brute force of that row (small integers: fp64 exact), in a
+    # batch whose rows differ, so a wrong batch stride or row mix-up changes the result
+    B = 5
+    x = np.stack([hcgen.uniform_int(8100 + b, 0, 1 << D, -40, 40) for b in range(B)]).astype(np.float64)
+    y = np.stack([hcgen.uniform_int(8100 + b, 1, 1 << D, -40, 40) for b in range(B)]).astype(np.float64)
+    z = orc.conv_batched(x, y)
+    assert z.shape == (B, 3 ** D)
+    for b in range(B):
+        want = brute_force(x[b].astype(np.int64), y[b].astype(np.int64), D)
+        assert z[b].tolist() == [float(v) for v in want], f"batch row {b}"
+
+
+def test_batched_f64_closed_forms(orc):
+    # row b: x = c_b * ones, y = d_b * ones -> z = c_b d_b 2^{#1}; row-specific scales pin the
+    # batch stride; powers of two keep every product and sum exact in fp64
+    D, B = 7, 4
+    scale_x = np.array([1.0, 2.0, 0.5, 4.0])
+    scale_y = np.array([1.0, 0.25, 8.0, 2.0])
+    x = scale_x[:, None] * np.ones((B, 1 << D))
+    y = scale_y[:, None] * np.ones((B, 1 << D))
+    z = orc.conv_batched(x, y)
+    base = _ones_closed_form(D).astype(np.float64)
+    for b in range(B):
+        assert np.array_equal(z[b], scale_x[b] * scale_y[b] * base)
+    # separable rows (integer factors in {1,2}: z <= 8^D exact in fp64 for D = 7)
+    fx, fy = hcgen.separable_factors(D, seed=1107, lo=1, hi=2)
+    xs = hcgen.tensor_product(fx).astype(np.float64)
+    ys = hcgen.tensor_product(fy).astype(np.float64)
+    zs = orc.conv_batched(np.stack([xs, ys]), np.stack([ys, xs]))
+    want = _separable_closed_form(fx, fy).astype(np.float64)
+    assert np.array_equal(zs[0], want) and np.array_equal(zs[1], want)  # commutativity across rows
+
+
+@pytest.mark.parametrize("D", [2, 3, 4])
+def test_cells_i64_bruteforce(orc, D):
+    # arbitrary cell order with repeats, out-of-order and the last cell, against the brute force
+    x = hcgen.uniform_int(8200 + D, 0, 1 << D, -(1 << 30), 1 << 30)
+    y = hcgen.uniform_int(8200 + D, 1, 1 << D, -(1 << 30), 1 << 30)
+    want = brute_force(x, y, D)
+    rng = np.random.default_rng(D)
+    ks = np.concatenate([rng.permutation(3 ** D), [3 ** D - 1, 0, 3 ** D - 1]]).astype(np.uint64)
+    got = orc.conv_cells(x, y, ks)
+    assert got.dtype == np.int64
+    for g, k in zip(got.tolist(), ks.tolist()):
+        e = want[int(k)]
+        assert (g - e) % (1 << 64) == 0 and g == ((e + (1 << 63)) % (1 << 64)) - (1 << 63)
+
+
+def test_cells_i64_closed_forms_large_D(orc):
+    # D = 18: sampled cells against the all-ones and separable closed forms (exact int64)
+    D = 18
+    rng = np.random.default_rng(18)
+    ks = rng.integers(0, 3 ** D, 4000, dtype=np.uint64)
+    ks[:3] = [0, 3 ** D - 1, (3 ** D - 1) // 2]          # corners and the all-ones-trit cell
+    x, y = hcgen.all_ones(D)
+    assert np.array_equal(orc.conv_cells(x, y, ks), _ones_closed_form(D)[ks.astype(np.int64)])
+    fx, fy = hcgen.separable_factors(D, seed=1118, lo=1, hi=2)
+    xs, ys = hcgen.tensor_product(fx), hcgen.tensor_product(fy)
+    want = _separable_closed_form(fx, fy)
+    assert np.array_equal(orc.conv_cells(xs, ys, ks), want[ks.astype(np.int64)])
