@@ -18,6 +18,7 @@
 #include "hc_common.cuh"
 #include "hc_tile.cuh"
 #include "hc_slab.cuh"
+#include "hc_slabx.cuh"
 
 using namespace hc;
 
@@ -202,6 +203,50 @@ cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const Sla
   return cudaGetLastError();
 }
 
+// warp-specialised engine (hc_slabx.cuh): one CTA of 640 threads per SM
+template <class T, int M>
+cudaError_t launch_slabx_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st,
+                           bool prep) {
+  auto kern = slabx_kernel<T, M>;
+  static int sms_cache[kMaxDev] = {};
+  int sms_scratch = 0;
+  int& sms = dev_slot(sms_cache, sms_scratch);
+  if (!sms) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SXCfg<T, M>::SMEM);
+    if (e != cudaSuccess) return e;
+    int occ = 0, dev = 0, n = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SX_NT, SXCfg<T, M>::SMEM);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    sms = n;
+  }
+  const uint64_t tiles = (uint64_t)a.nslab * upow3(M);
+  const unsigned grid = (unsigned)(tiles < (uint64_t)sms ? tiles : (uint64_t)sms);
+  cudaError_t e = cudaMemsetAsync(a.ctr, 0, sizeof(uint32_t) * (2 + 2 * (size_t)a.nslab), st);
+  if (e != cudaSuccess) return e;
+  if (prep) {
+    e = launch_prep<T, M>(x, y, xu, yu, a.k, st);
+    if (e != cudaSuccess) return e;
+  }
+  static const int lag_env = getenv("HC_SLABX_LAG") ? atoi(getenv("HC_SLABX_LAG")) : 2;
+  SlabxArgs sa{a.nslab, (uint32_t)(lag_env < 1 ? 1 : lag_env), a.ctr, a.order};
+  LaunchScope ls("slab", st);
+  kern<<<grid, SX_NT, SXCfg<T, M>::SMEM, st>>>(xu, yu, z, sa);
+  return cudaGetLastError();
+}
+
+// engine for the plain two-level convolution: "slabx" (warp-specialised, default) or the
+// fork-join "slab8" (HC_ENGINE=slab8); the fused-carry applications always use slab8
+inline bool use_slabx() {
+  static const int v = [] {
+    const char* s = getenv("HC_ENGINE");
+    return (s && std::string(s) == "slab8") ? 0 : 1;
+  }();
+  return v != 0;
+}
+
 template <class T>
 cudaError_t launch_slab8(const T* x, const T* y, T* z, T* xu, T* yu, int M, const SlabArgs& a, cudaStream_t st,
                          bool prep) {
@@ -214,6 +259,13 @@ cudaError_t launch_slab8(const T* x, const T* y, T* z, T* xu, T* yu, int M, cons
         case 13: return launch_slab8_m<T, 6, 3>(x, y, z, xu, yu, a, st, prep);
         default: return cudaErrorInvalidValue;
       }
+    }
+  }
+  if (use_slabx() && !a.debug_skip) {
+    switch (M) {
+      case 5: return launch_slabx_m<T, 5>(x, y, z, xu, yu, a, st, prep);
+      case 6: return launch_slabx_m<T, 6>(x, y, z, xu, yu, a, st, prep);
+      default: return cudaErrorInvalidValue;
     }
   }
   switch (M) {
