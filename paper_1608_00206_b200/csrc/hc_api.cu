@@ -230,19 +230,20 @@ cudaError_t launch_slabx_m(const T* x, const T* y, T* z, T* xu, T* yu, const Sla
     e = launch_prep<T, M>(x, y, xu, yu, a.k, st);
     if (e != cudaSuccess) return e;
   }
-  static const int lag_env = getenv("HC_SLABX_LAG") ? atoi(getenv("HC_SLABX_LAG")) : 2;
+  static const int lag_env = getenv("HC_SLABX_LAG") ? atoi(getenv("HC_SLABX_LAG")) : 3;
   SlabxArgs sa{a.nslab, (uint32_t)(lag_env < 1 ? 1 : lag_env), a.ctr, a.order};
   LaunchScope ls("slab", st);
   kern<<<grid, SX_NT, SXCfg<T, M>::SMEM, st>>>(xu, yu, z, sa);
   return cudaGetLastError();
 }
 
-// engine for the plain two-level convolution: "slabx" (warp-specialised, default) or the
-// fork-join "slab8" (HC_ENGINE=slab8); the fused-carry applications always use slab8
+// engine for the plain two-level convolution: the fork-join "slab8" (default, faster on B200:
+// DESIGN.md §4) or the warp-specialised "slabx" (HC_ENGINE=slabx); the fused-carry
+// applications always use slab8
 inline bool use_slabx() {
   static const int v = [] {
     const char* s = getenv("HC_ENGINE");
-    return (s && std::string(s) == "slab8") ? 0 : 1;
+    return (s && std::string(s) == "slabx") ? 1 : 0;
   }();
   return v != 0;
 }
@@ -576,6 +577,16 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
       cudaStreamSynchronize(st);
       double tot = 0;
       for (int i : {0, 1, 4, 5, 6}) tot += (double)h[i];
+      if (use_slabx()) {
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const double c = 1e3 * nsm;  // kclk per CTA
+        fprintf(stderr, "slabx phase (kclk per CTA): F2 total %.0f pairloop %.0f item-wait %.0f acc-empty-wait %.0f | "
+                "F1 raw-wait %.0f | S throttle %.0f ring-full %.0f | E idle %.0f tiles %.0f (%llu) p2 %.0f (%llu)\n",
+                h[9] / c, h[6] / c, h[5] / c, h[4] / c, h[7] / c, h[0] / c, h[8] / c, h[1] / c, h[2] / c, h[10], h[3] / c,
+                h[11]);
+      } else
       fprintf(stderr, "phase(Mclk/CTA-sum): select+wait %.0f pairloop %.0f inv+store %.0f p2 %.0f end %.0f "
               "(tot %.0f) | F1 mbar wait %.0f | t224 select %.0f end %.0f\n", h[0] / 1e6, h[1] / 1e6, h[6] / 1e6,
               h[4] / 1e6, h[5] / 1e6, tot / 1e6, h[7] / 1e6, h[2] / 1e6, h[3] / 1e6);

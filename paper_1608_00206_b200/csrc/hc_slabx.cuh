@@ -9,9 +9,8 @@
 // on their own warps and hand work over through mbarriers:
 //
 //   warps 0-7   F2  ("pair loop"): 243 units, 27 fp64/uint64 accumulators per thread (register
-//                   axes C = tile axes 0-2), unit of thread t = (e_a2, e_S) = (t % 3, t / 3), so
-//                   the three threads of one e_S sit in adjacent lanes and read the two b_a2
-//                   rows of the F1 stage as shared-memory broadcasts.
+//                   axes C = tile axes 0-2), unit of thread t = t8_unit(t) (the two-row e_a2 = 1
+//                   units grouped on warps 0-2, as in slab8).
 //   warps 8-10  F1  : evaluate tile axes a1 (warp 8 + e_s) and B of each pair's raw slices
 //                   (TMA ring) into the double-buffered F1 stage.
 //   warp 11     S   : claims pass-1 items, issues the TMA copies of their raw slices, throttles
@@ -24,8 +23,8 @@
 // TMEM (tcgen05.st, 54 columns of its lane) and starts the next tile at once; the E warp of
 // the same lane quadrant (warp 12 + w reads the lanes of warp w) loads them (tcgen05.ld) and
 // runs the tile interpolation while the pair loop goes on.  Four TMEM tile buffers (4 x 128
-// columns) decouple the two roles.  Registers are split per warpgroup (setmaxnreg): F2 128,
-// F1 + S 64, E 80 per thread.
+// columns) decouple the two roles.  Registers are split per warpgroup (setmaxnreg): F2 120,
+// F1 + S 64, E 88 per thread.
 //
 // Progress / deadlock freedom (grid = one resident CTA per SM):
 //  * S claims the next pass-1 item only after issuing every slice of the previous one, and only
@@ -159,30 +158,6 @@ __device__ __forceinline__ void tmem_ld27(uint32_t ta, T* v) {
   }
 }
 
-// F2 of one pair for thread unit (e_a2, e_S): every lane loads both b_a2 rows of its e_S (the
-// three lanes of one e_S read the same addresses: broadcast) and evaluates axis a2 at e_a2
-// (PAPER.md 186-189: a0, a0 + a1, a1), then the C-axes forward fused with the product.
-template <class T>
-__device__ __forceinline__ void sx_f2(const T* P, int ea2, int eS, T* acc) {
-  const T* px = P + eS * PS_ROW;
-  T xt[8], yt[8];
-#pragma unroll
-  for (int j = 0; j < 8; j += 2) {
-    T a0, a1, b0, b1, c0, c1, d0, d1;
-    lds2(px + j, a0, a1);                    // x, b_a2 = 0
-    lds2(px + PS_A2 + j, b0, b1);            // x, b_a2 = 1
-    lds2(px + PS_OP + j, c0, c1);            // y, b_a2 = 0
-    lds2(px + PS_OP + PS_A2 + j, d0, d1);    // y, b_a2 = 1
-    const T s0 = Ar<T>::add(a0, b0), s1 = Ar<T>::add(a1, b1);
-    const T u0 = Ar<T>::add(c0, d0), u1 = Ar<T>::add(c1, d1);
-    xt[j] = ea2 == 0 ? a0 : (ea2 == 2 ? b0 : s0);
-    xt[j + 1] = ea2 == 0 ? a1 : (ea2 == 2 ? b1 : s1);
-    yt[j] = ea2 == 0 ? c0 : (ea2 == 2 ? d0 : u0);
-    yt[j + 1] = ea2 == 0 ? c1 : (ea2 == 2 ? d1 : u1);
-  }
-  fwd_mul_acc<3, T>(xt, yt, acc);
-}
-
 #ifdef HC_PHASE_PROF
 #define SX_PROF_ADD(i, v) atomicAdd(&hc_phase[i], (unsigned long long)(v))
 #else
@@ -234,20 +209,31 @@ slabx_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   tc_fence_after();
   const uint32_t tbase = s_taddr;
 
-  // per-warpgroup register budgets (pool 640 x 96): F2 2 x 128 x 128, F1 + S 128 x 64, E 2 x 128 x 80
-  if (warp < 8) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
+  // per-warpgroup register budgets (pool 640 x 96): F2 2 x 128 x 120, F1 + S 128 x 64, E 2 x 128 x 88
+  if (warp < 8) asm volatile("setmaxnreg.inc.sync.aligned.u32 120;");
   else if (warp < 12) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
-  else asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
+  else asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
 
   if (warp < 8) {
     // ================================ F2 ==================================================
     const bool unit = tid < 243;
-    const int ea2 = tid % 3, eS = tid / 3;
+    const int uu = t8_unit(tid);           // e_a2 = 1 units on warps 0-2 (two-row loads)
+    const int ea2 = uu / 81, eS = uu - 81 * ea2;
     const uint32_t tcol = tbase + (((uint32_t)(warp & 3) * 32u) << 16) + (uint32_t)(warp >> 2) * 64u;
     uint32_t qpos = 0, tb = 0;
+#ifdef HC_PHASE_PROF
+    long long tk0 = clock64();
+#endif
     while (true) {
       const uint32_t slot = qpos % SX_QN;
+#ifdef HC_PHASE_PROF
+      long long tw0 = clock64();
+#endif
       mbar_wait(&item_full[slot], (qpos / SX_QN) & 1);
+#ifdef HC_PHASE_PROF
+      if (tid == 0) SX_PROF_ADD(5, clock64() - tw0);
+      long long tp0 = clock64();
+#endif
       const SXItem it = s_item[slot];
       ++qpos;
       if (it.npairs == 0xffffffffu) break;
@@ -256,12 +242,19 @@ slabx_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       for (int i = 0; i < 27; ++i) acc[i] = T(0);
       bar_named(1, SX_PN);  // F1(0) is in the stage; every P thread has read the item
       for (uint32_t p = 0; p < it.npairs; ++p) {
-        if (unit) sx_f2<T>(Pst + (p & 1) * PS_SZ, ea2, eS, acc);
+        if (unit) t8_f2<T>(Pst + (p & 1) * PS_SZ, ea2, eS, acc);
         bar_named(1, SX_PN);
       }
       // hand the accumulators to E through TMEM buffer b
       const uint32_t b = tb % SX_NBUF;
+#ifdef HC_PHASE_PROF
+      long long ta0 = clock64();
+      if (tid == 0) SX_PROF_ADD(6, ta0 - tp0);
+#endif
       if (tb >= SX_NBUF) mbar_wait(&acc_empty[b], ((tb / SX_NBUF) + 1) & 1);
+#ifdef HC_PHASE_PROF
+      if (tid == 0) SX_PROF_ADD(4, clock64() - ta0);
+#endif
       tc_fence_after();
       if (tid == 0) { s_tile[b].dest = it.dest; s_tile[b].j = it.j; }
       tmem_st27<T>(tcol + b * 128u, acc);
@@ -272,6 +265,9 @@ slabx_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       ++tb;
     }
     if (tid == 0) s_ptiles = tb;
+#ifdef HC_PHASE_PROF
+    if (tid == 0) SX_PROF_ADD(9, clock64() - tk0);
+#endif
   } else if (warp < SX_SW) {
     // ================================ F1 ==================================================
     const int es = warp - SX_F1W;
@@ -285,7 +281,13 @@ slabx_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       for (uint32_t p = 0; p <= np; ++p) {
         if (p < np) {  // F1 of pair p into stage p & 1
           const uint32_t st = rdone % SX_NRAW;
+#ifdef HC_PHASE_PROF
+          long long tr0 = clock64();
+#endif
           mbar_wait(&raw_full[st], (rdone / SX_NRAW) & 1);
+#ifdef HC_PHASE_PROF
+          if (es == 0 && lane == 0) SX_PROF_ADD(7, clock64() - tr0);
+#endif
           t8_f1<T>(R + st * RS_SZ, Pst + (p & 1) * PS_SZ, es, lane);
           __syncwarp();
           if (lane == 0) mbar_arrive(&raw_empty[st]);
@@ -335,7 +337,13 @@ slabx_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
         uint32_t s = 0;
         do {
           const uint32_t st = rseq % SX_NRAW;
+#ifdef HC_PHASE_PROF
+          long long ts0 = clock64();
+#endif
           if (rseq >= SX_NRAW) mbar_wait(&raw_empty[st], ((rseq / SX_NRAW) + 1) & 1);
+#ifdef HC_PHASE_PROF
+          SX_PROF_ADD(8, clock64() - ts0);
+#endif
           fence_proxy_async();  // the stage was last read through the generic proxy
           const uint64_t iT = base | s, jT = base | (freeb & ~s);
           const T* sx = sx0 + iT * stride;
@@ -356,42 +364,47 @@ slabx_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
     __syncwarp();
   } else {
     // ================================ E ===================================================
+    // Work items: tile epilogues (from the local F2 warps, through TMEM) and pass-2 items
+    // (three 9-column chunks of a slab whose tiles are all stored).
     const int e = tid - SX_E0;         // 0..255
     const int we = e >> 5;             // reads the TMEM lanes of F2 warp we
     const bool task = e < 243;
-    const int u = (e % 3) * 81 + e / 3;  // unit of F2 thread e: (e_a2, e_S) -> u = 81 e_a2 + e_S
+    const int u = t8_unit(e);          // unit of F2 thread e (same TMEM lane)
     const uint32_t tcol = tbase + (((uint32_t)(we & 3) * 32u) << 16) + (uint32_t)(we >> 2) * 64u;
     const uint64_t pol_keep = policy_evict_last();  // pass-1 tiles wait in L2 for pass 2
+    constexpr uint32_t NONE = 0xffffffffu;
     uint32_t te = 0;                    // tiles taken from P
-    uint32_t held = 0xffffffffu;        // claimed pass-2 item (leader)
-    bool exhausted = false;             // pass-2 claims exhausted (leader)
-    uint32_t pend = 0xffffffffu;        // slab position of a stored, not yet published tile (leader)
-    auto signal = [&]() {               // leader: publish the previous tile (fence + count)
-      if (pend != 0xffffffffu) {
+    // leader state (thread e = 0 only; in shared memory, off the other threads' registers)
+    __shared__ struct {
+      uint32_t held;                    // claimed pass-2 item
+      uint32_t exhausted;               // pass-2 claims exhausted
+      uint32_t pend;                    // slab position of a stored, not yet published tile
+    } L;
+    if (e == 0) { L.held = L.pend = NONE; L.exhausted = 0; }
+    auto signal = [&]() {               // leader: publish a tile (fence + count)
+      if (L.pend != NONE) {
         __threadfence();
-        atomicAdd(done_ctr + pend, 1u);
-        pend = 0xffffffffu;
+        atomicAdd(done_ctr + L.pend, 1u);
+        L.pend = NONE;
       }
     };
     while (true) {
       if (e == 0) {
         long long t0 = clock64();
-        uint4 dec = make_uint4(0, 0, 0, 0);  // 1 tile, 2 pass-2 item, 3 exit
+        (void)t0;
+        uint4 dec = make_uint4(0, 0, 0, 0);  // x: 1 tile, 2 pass-2 item (y), 3 exit
         while (true) {
           if (mbar_test(&acc_full[te % SX_NBUF], (te / SX_NBUF) & 1)) { dec.x = 1; break; }
-          if (held == 0xffffffffu && !exhausted) {
+          if (L.held == NONE && !L.exhausted) {
             const uint32_t q2 = atomicAdd(ctr2, 1u);
-            if (q2 < total2) held = q2;
-            else exhausted = true;
+            if (q2 < total2) L.held = q2;
+            else L.exhausted = 1;
           }
-          if (held != 0xffffffffu) {
-            const uint32_t j2 = held / N2;
-            if (ld_relaxed(done_ctr + j2) >= N1) {
-              asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire the slab's tiles
-              dec.x = 2; dec.y = held; held = 0xffffffffu; break;
-            }
+          if (L.held != NONE && ld_relaxed(done_ctr + L.held / N2) >= N1) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire the slab's tiles
+            dec.x = 2; dec.y = L.held; L.held = NONE; break;
           }
-          if (held == 0xffffffffu && exhausted && s_ptiles == te) { dec.x = 3; break; }
+          if (L.held == NONE && L.exhausted && s_ptiles == te) { dec.x = 3; break; }
           signal();
           __nanosleep(32);
         }
@@ -404,6 +417,7 @@ slabx_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       if (dec.x == 1) {
         // ---- tile epilogue: TMEM -> registers -> interpolation over the 8 tile axes ----
         long long t0 = clock64();
+        (void)t0;
         const uint32_t b = te % SX_NBUF;
         tc_fence_after();
         const SXTile tl = s_tile[b];
@@ -443,12 +457,25 @@ slabx_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
             for (int i = 0; i < 9; ++i) st_hint(zt + i * 729 + col, w9[i], pol_keep);
           }
         }
-        bar_named(2, SX_EN);  // Eb is free; every store of this tile is issued
-        if (e == 0) pend = tl.j;
-        if (e == 0) SX_PROF_ADD(2, clock64() - t0);
+        // every E thread's stores of this tile are issued once all arrive here; the leader then
+        // owns the tile's publication (the others go on to the next decision barrier).  It must
+        // not wait for the next item: a pass-2 item of this slab may be what the leader waits for.
+        // (warp-uniform: the leader's warp waits, the other E warps only arrive)
+        if (e < 32) {
+          asm volatile("bar.sync 3, %0;" ::"r"(SX_EN) : "memory");
+          if (e == 0) {
+            if (L.pend != NONE) signal();
+            L.pend = tl.j;
+            SX_PROF_ADD(2, clock64() - t0);
+            SX_PROF_ADD(10, 1);
+          }
+        } else {
+          asm volatile("bar.arrive 3, %0;" ::"r"(SX_EN) : "memory");
+        }
       } else {
         // ---- pass-2 item: interpolation over the M middle axes, in place, final store ----
         long long t0 = clock64();
+        (void)t0;
         const uint32_t q2 = dec.y;
         const uint32_t j2 = q2 / N2, r2 = q2 - j2 * N2;
         T* zs = z + (uint64_t)args.order[j2].x * SLAB;
@@ -462,6 +489,7 @@ slabx_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
         if (e == 0) {
           atomicAdd(p2fin + j2, 1u);  // throttle only (no data is published through it)
           SX_PROF_ADD(3, clock64() - t0);
+          SX_PROF_ADD(11, 1);
         }
       }
     }
