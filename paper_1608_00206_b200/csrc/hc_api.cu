@@ -381,9 +381,15 @@ struct hc_plan_s {
 
 // Equal-cost contiguous split of the 3^k output slabs over ngpu ranks.  Cost of slab
 // t_T ~ alpha + 2^{#1(t_T)}: one unit per direct-split pair (PAPER.md 166-177) plus alpha
-// for the slab's interpolation and store.
+// for the slab's interpolation and store, in units of one pair.  alpha is fitted from shards
+// timed alone on a B200 (tools/shard_times.py, profiles/r02_shard_balance.txt);
+// HC_SHARD_ALPHA overrides it (calibration runs).
+static double shard_alpha() {
+  static const double a = getenv("HC_SHARD_ALPHA") ? atof(getenv("HC_SHARD_ALPHA")) : 13.0;
+  return a;
+}
 static std::vector<uint64_t> compute_cuts(int k, int ngpu) {
-  const double alpha = 1.0;
+  const double alpha = shard_alpha();
   const uint64_t n = upow3(k);
   std::vector<double> pref(n + 1, 0.0);
   for (uint64_t t = 0; t < n; ++t) {

@@ -56,12 +56,15 @@ def test_plan_without_device_fails_loudly(hc):
     assert ei.value.code == 5
 
 
+ALPHA = 13.0  # compute_cuts' fixed cost per slab, in pairs (fitted: profiles/r02_shard_balance.txt)
+
+
 def _slab_cost(t, k):
     ones = 0
     for _ in range(k):
         ones += t % 3 == 1
         t //= 3
-    return 1 + 2 ** ones
+    return ALPHA + 2 ** ones
 
 
 def _unit_axes(D):
@@ -90,7 +93,7 @@ def test_shard_ranges_partition(hc, D, ngpu):
         k = D - s
         costs = [sum(_slab_cost(t, k) for t in range(b // tile, e // tile)) for b, e in ranges]
         ideal = sum(costs) / ngpu
-        assert max(costs) - ideal <= 1 + 2 ** k
+        assert max(costs) - ideal <= ALPHA + 2 ** k
 
 
 def test_shard_errors(hc):
