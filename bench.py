@@ -76,13 +76,48 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(workload):
+def csrc_sha():
+    """sha256 over the CUDA sources of libhc.so: a captured DRAM-traffic figure is only reused
+    for the exact kernel code it was captured on."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted(glob.glob(os.path.join(ROOT, "paper_1608_00206_b200", "csrc", "*"))):
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def load_traffic(key):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
+    ncu --set full capture of this exact workload / variant / kernel on this exact source
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py); else (None, reason)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        return d.get(workload)
-    return None
+    if not os.path.exists(p):
+        return None, "no capture"
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(key)
+    if not isinstance(e, dict):
+        return None, f"no capture for {key}"
+    if e.get("csrc_sha") != csrc_sha():
+        return None, f"capture for {key} is of other kernel sources ({e.get('csrc_sha')})"
+    return e.get("bytes_per_launch"), e.get("source")
+
+
+# int32 lane-instructions per output entry of the int64 (wrapping uint64) engines, from the
+# kernels' arithmetic: 64-bit add / sub = 2 instructions, multiply-add mod 2^64 = 5; pair loop per
+# tile = 243 units x (27 mad + 38 add) + 81 x 16 row sums + 96 F1 lanes x 19 adds + 32 x 8
+# (cf. the fp64 model below), x (4/3)^k direct-split pairs; interpolation 2/3 sub per output
+# and axis.  Peak: the fma and alu pipes each issue one warp instruction per 2 clk per SM
+# sub-partition (B300_MICROARCH.md "Pipe rates") = 128 int32 lanes/clk/SM x 148 SMs at the
+# 1965 MHz max clock = 37.2 T/s (derived, not measured).
+INT32_PEAK = 148 * 128 * 1.965e9
+
+
+def int_ops_per_output(D, k_top, interp_axes):
+    pair = (243 * (27 * 5 + 38 * 2) + 81 * 16 * 2 + 96 * 19 * 2 + 32 * 8 * 2) / 6561.0
+    return pair * (4.0 / 3.0) ** k_top + (4.0 / 3.0) * interp_axes
 
 
 class ClockSampler:
@@ -196,6 +231,29 @@ def oracle_sample_rate(wl, budget_s=10.0, seed=99):
                                       f"form, avg (4/3)^{D} pairs per cell)"), total_t
 
 
+def config_dict(wl, args, world, flush=None):
+    """The `config` object of the JSON line; identical for the repo arm and --impl reference."""
+    w = WORKLOADS[wl]
+    D = w["D"]
+    n_total = w.get("B", 1) * 3 ** D
+    in_bytes = 2 * w.get("B", 1) * 2 ** D * 8
+    if flush is None:
+        flush = n_total * 8 + in_bytes < 2 * L2_BYTES
+    return {
+        "workload": wl, "desc": w["desc"], "D": D, "output_entries": n_total,
+        "variant": w.get("app", args.variant),
+        "parallelism": (f"evalpoint k={args.ep_k} x{world} (all-to-all)" if args.variant == "evalpoint"
+                        else f"evalpoint k={args.ep_k} x{world} (peer reads)" if args.variant == "evalpoint-peer"
+                        else (f"{args.vshards} output-split shards streamed through one buffer, "
+                              f"{args.vshards // world} per rank x{world}" if wl == "c5_d22_f64"
+                              else (f"output-split x{world}" if world > 1 else "single"))),
+        "l2": ("L2 flushed between steps (%d MB write, untimed), each step timed alone" % (4 * L2_BYTES >> 20)
+               if flush else
+               "output (%.2f GB) > 2 x L2 (126 MB): every step streams the whole output" % (n_total * 8 / 1e9)),
+        "min_bytes_per_step": n_total * 8 + in_bytes,
+    }
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -217,7 +275,7 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * n_entries / v, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64" if "f64" in wl else "int64", "data": "synthetic",
-        "config": {"workload": wl, "desc": w["desc"], "D": w["D"], "output_entries": n_entries},
+        "config": config_dict(wl, args, world),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
                          "cpu": cpu_model()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -432,36 +490,68 @@ def main():
     ms_per_step = t_max / args.steps
     value = n_total / (ms_per_step / 1e3)
 
-    # roofline of the dominant kernel: algorithmic bytes per launch / avg launch time
+    # roofline of the dominant kernel: algorithmic bytes (or operations) per launch / avg launch time
     launches_per_step = kcount / max(args.steps, 1)
-    out_bytes_local = n_local * 8
-    in_bytes_local = in_bytes if not batched else in_bytes
-    alg_bytes_per_launch = (out_bytes_local + in_bytes_local * max(launches_per_step, 1)) / max(launches_per_step, 1)
+    lps = max(launches_per_step, 1)
     peak, peak_src = load_peaks()
+    evalpoint = args.variant in ("evalpoint", "evalpoint-peer") and "app" not in w and not batched
+    if evalpoint:
+        # the dominant launches are the per-point (D-k)-dimensional convolutions (slab engine)
+        Dl = D - args.ep_k
+        outs_per_launch = 3 ** Dl
+        alg_bytes_per_launch = float((3 ** Dl + 2 * 2 ** Dl) * 8)
+    else:
+        outs_per_launch = n_local / lps
+        alg_bytes_per_launch = (n_local * 8 + in_bytes * lps) / lps
     achieved = alg_bytes_per_launch / (k_avg / 1e3) / 1e9 if k_avg > 0 else None
-    traffic = load_traffic(wl)
+    tkey = f"{wl}|{w.get('app', args.variant)}|{prof_name}"
+    traffic, tsrc = load_traffic(tkey)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_source": tsrc,
                 "kernel": prof_name, "alg_bytes_per_launch": alg_bytes_per_launch, "launch_ms": k_avg,
-                "peak_source": peak_src,
+                "launches_per_step": launches_per_step, "peak_source": peak_src,
                 # the same efficiency against the 8.0 TB/s spec figure, and the
                 # DRAM traffic ncu measured for this launch (profiles/ncu_traffic.json) over its time
                 "frac_vs_spec_8000": (achieved / 8000.0) if achieved else None,
                 "dram_gbs": (traffic / (k_avg / 1e3) / 1e9) if (traffic and k_avg > 0) else None}
+    k_top = max(D - 14, 0) if D >= 13 else max(D - 8, 0)
+    interp = min(D, 14) if D >= 13 else min(D, 8)
+    if w.get("app") == "conv1d":
+        # f1: the 1-D convolution's output is 2^(D+1) - 1 entries (16.8 MB at D = 20), so the 3^D
+        # write is not in the algorithm; the fused kernel is bound by integer arithmetic
+        ops = int_ops_per_output(D, k_top, interp) * 3 ** D / lps
+        out_b = ((2 << D) - 1) * 8 + in_bytes
+        roofline = {"bound": "alu", "achieved": ops / (k_avg / 1e3) / 1e12 if k_avg else None,
+                    "peak": INT32_PEAK / 1e12, "unit": "T int32 lane-instr/s",
+                    "frac": (ops / (k_avg / 1e3) / INT32_PEAK) if k_avg else None,
+                    "ops_per_hypercube_output": int_ops_per_output(D, k_top, interp), "kernel": prof_name,
+                    "launch_ms": k_avg, "peak_source": "derived: 128 int32 lanes/clk/SM x 148 SMs x 1965 MHz",
+                    "traffic": traffic, "traffic_source": tsrc,
+                    "hbm_min_bytes_frac": (out_b / (k_avg / 1e3) / 1e9 / peak) if k_avg else None}
     # fp64 co-roofline of the two-level engine (DESIGN.md §4 cost model): algorithmic fp64
     # instructions per output entry = pair loop (F2 27 FMA + 38 add per unit and pair, 16 row
     # sums on the e_a2 = 1 units, F1 19 adds (+8) per lane) x (4/3)^k pairs + 2/3 per
-    # interpolated axis (tile and middle axes); against the measured DADD/DFMA lane rate
+    # interpolated axis (tile and middle axes); against the measured DADD/DFMA lane rate.
+    # int64 workloads: the int32-instruction model above against the derived INT peak.
     co = None
-    if tdt == torch.float64 and prof_name == "slab" and D >= 13:
-        k_top = D - 14 if D >= 14 else 0
+    Dk = D - args.ep_k if evalpoint else D
+    ktop_k = (max(Dk - 14, 0) if Dk >= 13 else max(Dk - 8, 0))
+    interp_k = min(Dk, 14) if Dk >= 13 else min(Dk, 8)
+    if tdt == torch.float64 and w.get("app") != "conv1d":
         pair_ops = (243 * (27 + 38) + 81 * 16 + 96 * 19 + 32 * 8) / 6561.0
-        ops_per_out = pair_ops * (4.0 / 3.0) ** k_top + (2.0 / 3.0) * min(D, 14)
-        ops = ops_per_out * n_local / max(launches_per_step, 1)
+        ops_per_out = pair_ops * (4.0 / 3.0) ** ktop_k + (2.0 / 3.0) * interp_k
+        ops = ops_per_out * outs_per_launch
         fp64_peak = 17.5e12  # fp64 lane-instructions/s measured on this B200 (DFMA 17.0, DADD 18.5 T/s)
         co = {"bound": "fp64", "ops_per_output": ops_per_out, "achieved": ops / (k_avg / 1e3) / 1e12 if k_avg else None,
               "peak": fp64_peak / 1e12, "unit": "T fp64 instr-lanes/s",
               "frac": (ops / (k_avg / 1e3) / fp64_peak) if k_avg else None}
+    elif tdt == torch.int64 and w.get("app") != "conv1d":
+        ops_per_out = int_ops_per_output(Dk, ktop_k, interp_k)
+        ops = ops_per_out * outs_per_launch
+        co = {"bound": "int", "ops_per_output": ops_per_out,
+              "achieved": ops / (k_avg / 1e3) / 1e12 if k_avg else None, "peak": INT32_PEAK / 1e12,
+              "unit": "T int32 lane-instr/s", "frac": (ops / (k_avg / 1e3) / INT32_PEAK) if k_avg else None,
+              "peak_source": "derived: 128 int32 lanes/clk/SM x 148 SMs x 1965 MHz"}
 
     # end to end through the host-buffer C-ABI entry point (pinned host memory, copies inside)
     e2e = None
@@ -495,18 +585,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64" if tdt == torch.float64 else "int64",
             "data": "synthetic",
-            "config": {"workload": wl, "desc": w["desc"], "D": D, "output_entries": n_total,
-                       "variant": w.get("app", args.variant),
-                       "parallelism": (f"evalpoint k={args.ep_k} x{world} (all-to-all)" if args.variant == "evalpoint"
-                                       else f"evalpoint k={args.ep_k} x{world} (peer reads)" if args.variant == "evalpoint-peer"
-                                       else (f"{args.vshards} output-split shards streamed through one buffer, "
-                                             f"{args.vshards // world} per rank x{world}" if wl == "c5_d22_f64"
-                                             else (f"output-split x{world}" if world > 1 else "single"))),
-                       "l2": ("L2 flushed between steps (%d MB write, untimed), each step timed alone" % (4 * L2_BYTES >> 20)
-                              if flush else
-                              "output (%.2f GB) > 2 x L2 (126 MB): every step streams the whole output"
-                              % (n_total * 8 / 1e9)),
-                       "min_bytes_per_step": n_total * 8 + in_bytes},
+            "config": config_dict(wl, args, world, flush),
             "hbm_gbs_min_bytes": (n_total * 8 + in_bytes) / (ms_per_step / 1e3) / 1e9,
             "roofline": roofline, "co_roofline": co, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,

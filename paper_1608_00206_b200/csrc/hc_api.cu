@@ -319,6 +319,32 @@ cudaError_t launch_tile(const T* x, const T* y, T* z, int D, uint64_t slab0, uin
   }
 }
 
+// single pair, 9 <= D <= 12: the 3^8-tile engine gives only 3^(D-8) CTAs (9 at D = 10, BASELINE
+// config 1).  Optionally (HC_SMALL_L = 5..7) the work is cut into smaller tiles of L' < 8 axes,
+// one CTA each (tile_kernel); unit u of 3^8 outputs = sub-tiles [u 3^(8-L'), (u+1) 3^(8-L')).
+// Measured on B200 (L2 flushed, int64, us for D = 9/10/11/12): L' = 5: 18/31/49/88, 6: 12/16/25/43,
+// 7: 10/14/21/37, 8: 10/12/16/25 -- more, smaller CTAs lose to the TMA-fed 3^8 tiles, so the
+// default stays L' = 8 (profiles/r02_small_d_tiles.txt).
+template <class T>
+cudaError_t launch_tile_small(const T* x, const T* y, T* z, int D, int L, uint64_t u0, uint64_t nu, cudaStream_t st) {
+  const uint64_t f = upow3(8 - L);
+  const uint64_t nslab = upow3(D - L);
+  switch (L) {
+    case 5: return launch_tile_cfg<T, 3, 2, 0>(x, y, z, D, u0 * f, nslab, nu * f, st);
+    case 6: return launch_tile_cfg<T, 3, 3, 0>(x, y, z, D, u0 * f, nslab, nu * f, st);
+    case 7: return launch_tile_cfg<T, 3, 3, 1>(x, y, z, D, u0 * f, nslab, nu * f, st);
+    default: return launch_tile8<T>(x, y, z, D, u0, upow3(D - 8), nu, st);
+  }
+}
+
+// tile axes L' for a single-pair D in 9..12 (HC_SMALL_L overrides; 8 = the 3^8-tile engine)
+int small_tile_axes(int D) {
+  static const int env = getenv("HC_SMALL_L") ? atoi(getenv("HC_SMALL_L")) : 0;
+  if (env >= 5 && env <= 8) return env;
+  (void)D;
+  return 8;
+}
+
 cudaError_t launch_any(hc_dtype dt, const void* x, const void* y, void* z, int D, uint64_t slab0,
                        uint64_t nslab, uint64_t nitems, cudaStream_t st) {
   if (dt == HC_INT64)
@@ -553,7 +579,15 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
   const Geometry& g = p->g;
   cudaError_t e;
   if (!g.two_level) {
-    e = launch_any(p->dtype, x, y, z, p->D, u0, g.nunits, u1 - u0, st);
+    const int Ls = (p->D >= 9 && p->D <= 12) ? small_tile_axes(p->D) : 8;
+    if (Ls < 8) {
+      if (p->dtype == HC_INT64)
+        e = launch_tile_small<uint64_t>((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)z, p->D, Ls, u0, u1 - u0, st);
+      else
+        e = launch_tile_small<double>((const double*)x, (const double*)y, (double*)z, p->D, Ls, u0, u1 - u0, st);
+    } else {
+      e = launch_any(p->dtype, x, y, z, p->D, u0, g.nunits, u1 - u0, st);
+    }
   } else {
     const uint4* order = slab_order(p, u0, u1);
     if (!order) return HC_ERR_CAPACITY;

@@ -502,6 +502,18 @@ def test_engine_variants_by_env(env):
         "zb = torch.empty((5, 6561), dtype=torch.int64, device='cuda')\n"
         "hc.convolve_batched(torch.from_numpy(xb).cuda(), torch.from_numpy(yb).cuda(), zb)\n"
         "torch.cuda.synchronize(); assert np.array_equal(zb.cpu().numpy(), oracle.conv_batched(xb, yb))\n"
+        "D = 17\n"  # k = 3 top axes: 27 slabs, 3-way shards concatenate to the full output
+        "x, y = hcgen.make_pair(D, 'float64', 'exp_norm', 7117)\n"
+        "xg, yg = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()\n"
+        "z = torch.empty(3 ** D, dtype=torch.float64, device='cuda'); hc.Plan(D, 'float64').convolve(xg, yg, z)\n"
+        "parts = []\n"
+        "for r in range(3):\n"
+        "    p = hc.Plan(D, 'float64', 3, r); b, e = p.shard_info()\n"
+        "    zs = torch.empty(e - b, dtype=torch.float64, device='cuda'); p.convolve_sharded(xg, yg, zs); parts.append(zs)\n"
+        "torch.cuda.synchronize(); assert torch.equal(torch.cat(parts), z)\n"
+        "ks = np.random.default_rng(17).integers(0, 3 ** D, 20000)\n"
+        "err = np.max(np.abs(z[torch.from_numpy(ks).cuda()].cpu().numpy() - oracle.conv_cells(x, y, ks.astype(np.uint64))))\n"
+        "assert err <= 1e-12, err\n"
         "print('ok')\n")
     env = dict(os.environ, **env)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
