@@ -597,7 +597,15 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
     // pass-2 items of j - T8_RING, which must be claimed earlier: lag <= T8_RING - 1
     uint32_t lg = (uint32_t)(lag < 1 ? 1 : lag);
     if (ring && lg > T8_RING - 1) lg = T8_RING - 1;
-    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg, lg, cout, ring};
+    static const int keep = getenv("HC_KEEP_POLICY") ? atoi(getenv("HC_KEEP_POLICY")) : 0;
+    static const int persist_mb = [] {
+      const int mb = getenv("HC_L2_PERSIST_MB") ? atoi(getenv("HC_L2_PERSIST_MB")) : 0;
+      if (mb > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mb << 20);
+      return mb;
+    }();
+    (void)persist_mb;
+    static const int p2pf = getenv("HC_P2_PREFETCH") ? atoi(getenv("HC_P2_PREFETCH")) : 0;
+    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg, lg, cout, ring, keep, p2pf};
 #ifdef HC_PHASE_PROF
     {
       unsigned long long zero[16] = {0};

@@ -30,6 +30,16 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_unchanged() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -481,6 +491,33 @@ __device__ __forceinline__ constexpr int bitval3(int e) {  // sum_b digit_b(e) 2
   for (int b = 0, p = 1; b < N; ++b, p <<= 1, e /= 3) v += (e % 3) * p;
   return v;
 }
+// Interpolation over N axes fused with the carry binning of f1: out[val] = sum over the 3^N
+// positions e with val(e) = sum_b e_b 2^b of the interpolated z[e] (PAPER.md 187-189 per axis,
+// 354-373 for the carries).  Axis by axis from the top: the three top-digit slices are binned
+// recursively (2^N - 1 coefficients each), interpolated as coefficient vectors (the
+// interpolation is linear and acts on the top digit only), and merged with weights 2^(N-1)
+// and 2^N.  Fewer live values than interpolating all 3^N first and binning afterwards.
+template <int N, class T>
+__device__ __forceinline__ void inv_bin(const T* v, T* out) {
+  if constexpr (N == 0) {
+    out[0] = v[0];
+  } else {
+    constexpr int m = ipow3(N - 1), L = (1 << N) - 1, h = 1 << (N - 1);
+    T a0[L], a1[L], a2[L];
+    inv_bin<N - 1, T>(v, a0);
+    inv_bin<N - 1, T>(v + m, a1);
+    inv_bin<N - 1, T>(v + 2 * m, a2);
+#pragma unroll
+    for (int i = 0; i < 2 * L + 1; ++i) out[i] = T(0);
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      out[i] = Ar<T>::add(out[i], a0[i]);                                       // digit 0: weight 0
+      out[i + h] = Ar<T>::add(out[i + h], Ar<T>::sub(Ar<T>::sub(a1[i], a0[i]), a2[i]));  // digit 1
+      out[i + 2 * h] = Ar<T>::add(out[i + 2 * h], a2[i]);                       // digit 2: weight 2^N
+    }
+  }
+}
+
 template <class T, int M, class Mid>
 __device__ __forceinline__ void p2_carry_chunk(const T* __restrict__ zs, uint32_t c, T* sm, int task,
                                                unsigned long long* __restrict__ out, uint64_t base, int sched,
@@ -513,11 +550,8 @@ __device__ __forceinline__ void p2_carry_chunk(const T* __restrict__ zs, uint32_
     T v[NHI];
 #pragma unroll
     for (int e = 0; e < NHI; ++e) v[e] = sm[e * P2S + el * P2W + pos];
-    inv_reg<HI, T>(v);
-#pragma unroll
-    for (int i = 0; i < NB; ++i) b[i] = T(0);
-#pragma unroll
-    for (int e = 0; e < NHI; ++e) b[bitval3<HI>(e)] += v[e];
+    static_assert(NB == (2 << HI) - 1, "bins of HI digits");
+    inv_bin<HI, T>(v, b);
   }
   __syncthreads();  // the exchange is reused below
   T* bs = sm;                    // [pos][vhi][e_lo]: 9 x NB x 27
@@ -584,7 +618,9 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   const uint32_t total = ns * (N1 + N2);
   const uint32_t lag = args.lag;
   const uint64_t pol_in = policy_evict_first();   // middle-axes tables are streamed
-  const uint64_t pol_keep = policy_evict_last();  // pass-1 tiles wait in L2 for pass 2
+  // pass-1 tiles wait in L2 for pass 2 (args.keep_policy: 0 evict_last, 1 evict_normal, 2 unchanged)
+  const uint64_t pol_keep = args.keep_policy == 1 ? policy_evict_normal()
+                            : (args.keep_policy == 2 ? policy_evict_unchanged() : policy_evict_last());
   const uint64_t stride = upow3(M) * 256;
   const bool skip1 = args.debug_skip == 2, skip2 = args.debug_skip == 1;
   T* R = sm + T8Cfg<T>::ALIAS;
@@ -802,6 +838,18 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
                                vcol + (vtop << (8 + M)), ch == 0 ? T8_SCHED : -1, signal);
         }
       } else {
+      if (args.p2_prefetch) {
+        // pull the item's later chunks into L2 while chunk 0 runs: part of the slab may have been
+        // evicted to HBM since pass 1 wrote it; one bulk L2 prefetch (TMA unit, no registers, no
+        // shared memory) per row of the item's P2W * T8_P2CH columns, 16-B aligned cover
+        constexpr int NROW = ipow3(M);
+        const uint64_t c0 = (uint64_t)it.r * (P2W * T8_P2CH);
+        for (int row = threadIdx.x; row < NROW; row += T8_NT) {
+          const uintptr_t a = reinterpret_cast<uintptr_t>(zs + (uint64_t)row * 6561ull + c0);
+          const uintptr_t lo = a & ~(uintptr_t)15, hi = (a + 8 * P2W * T8_P2CH + 15) & ~(uintptr_t)15;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
+        }
+      }
 #pragma unroll 1
       for (int ch = 0; ch < T8_P2CH; ++ch) {
         if (ch) __syncthreads();  // the exchange buffer is rewritten by the next chunk

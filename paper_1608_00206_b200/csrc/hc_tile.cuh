@@ -271,6 +271,8 @@ struct SlabArgs {
   uint32_t lag;        // pass 2 of slab j is scheduled after pass 1 of slab j + lag (>= 1)
   unsigned long long* cout;  // slab8_kernel<uint64_t, M, 2>: carry bins (f1), else unused
   void* ring;                // slab8_kernel<uint64_t, M, 2>: T8_RING slab buffers for pass-1 tiles
+  int keep_policy;           // L2 policy of the pass-1 tile stores (0 evict_last, 1 evict_normal, 2 unchanged)
+  int p2_prefetch;           // pass-2 items bulk-prefetch their columns into L2 (0 / 1)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
