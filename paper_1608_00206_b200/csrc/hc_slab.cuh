@@ -330,7 +330,7 @@ __device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, Raw
   }
   __syncthreads();
   if (unit) {  // unit (e_A, k_C): interpolate the B axes
-    const int a = tid / 27, c = tid - 27 * a;
+    const int c = tid / 9, a = tid - 9 * c;  // e_A fastest: conflict-free (stride 729 = 9 mod 16)
     T v[27];
 #pragma unroll
     for (int e = 0; e < 27; ++e) v[e] = S[a * 729 + e * 27 + c];

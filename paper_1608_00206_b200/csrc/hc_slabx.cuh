@@ -436,7 +436,7 @@ slabx_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
         bar_named(2, SX_EN);
         if (e == 0) signal();  // previous tile: its stores have drained by now
         if (task) {
-          const int a = e / 27, c = e - 27 * a;
+          const int c = e / 9, a = e - 9 * c;  // e_A fastest: conflict-free (stride 729 = 9 mod 16)
 #pragma unroll
           for (int i = 0; i < 27; ++i) v[i] = Eb[a * 729 + i * 27 + c];
           inv_reg<3, T>(v);
