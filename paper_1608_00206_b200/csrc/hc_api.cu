@@ -605,7 +605,15 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
     }();
     (void)persist_mb;
     static const int p2pf = getenv("HC_P2_PREFETCH") ? atoi(getenv("HC_P2_PREFETCH")) : 0;
-    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg, lg, cout, ring, keep, p2pf};
+    // pass-2 interleave: H pass-1 items of slab j + lag, then the rest mixed with slab j's
+    // pass-2 items; H must leave a multiple of the N2 = 243 pass-2 items (3^M - H = 243 m)
+    static const long head_env = getenv("HC_P2_HEAD") ? atol(getenv("HC_P2_HEAD")) : -1;
+    uint32_t head = 0xffffffffu;
+    if (head_env >= 0 && !ring) {
+      const long n1 = (long)upow3(g.M), n2 = (long)(upow3(8) / (P2W * T8_P2CH));
+      if (head_env < n1 && (n1 - head_env) % n2 == 0) head = (uint32_t)head_env;
+    }
+    SlabArgs a{u0, (uint32_t)(u1 - u0), g.k, p->ctr[slot], order, dbg, lg, cout, ring, keep, p2pf, head};
 #ifdef HC_PHASE_PROF
     {
       unsigned long long zero[16] = {0};

@@ -438,8 +438,13 @@ struct ItemDec {
   bool p1;
   uint32_t j, r;
 };
-__device__ __forceinline__ ItemDec decode_item(uint32_t q, uint32_t ns, uint32_t N1, uint32_t N2, uint32_t lag) {
-  // order with lag G: P1(0..G-1) | [P1(j) P2(j-G)] for j = G..ns-1 | P2(ns-G..ns-1)
+__device__ __forceinline__ ItemDec decode_item(uint32_t q, uint32_t ns, uint32_t N1, uint32_t N2, uint32_t lag,
+                                               uint32_t head = 0xffffffffu) {
+  // order with lag G: P1(0..G-1) | [P1(j) P2(j-G)] for j = G..ns-1 | P2(ns-G..ns-1).  With
+  // head = H < N1, a group [P1(j) P2(j-G)] is H pass-1 items of position j, then the remaining
+  // N1 - H pass-1 items interleaved with the N2 pass-2 items of position j - G (ratio
+  // (N1 - H) / N2 : 1): slab j - G is then consumed while slab j is produced instead of after it
+  // (a smaller L2 footprint); every pass-2 item still follows all pass-1 items of its slab.
   ItemDec d;
   const uint32_t G = lag < ns ? lag : ns;
   if (q < G * N1) {
@@ -449,7 +454,12 @@ __device__ __forceinline__ ItemDec decode_item(uint32_t q, uint32_t ns, uint32_t
     const uint32_t pr = q2 / (N1 + N2);
     const uint32_t rr = q2 - pr * (N1 + N2);
     if (pr + G < ns) {
-      if (rr < N1) { d.p1 = true; d.j = pr + G; d.r = rr; }
+      if (head < N1 && rr >= head) {
+        const uint32_t per = (N1 - head) / N2;  // pass-1 items per pass-2 item (N2 divides N1 - head)
+        const uint32_t g = (rr - head) / (per + 1), o = (rr - head) - g * (per + 1);
+        if (o < per) { d.p1 = true; d.j = pr + G; d.r = head + g * per + o; }
+        else { d.p1 = false; d.j = pr; d.r = g; }
+      } else if (rr < N1) { d.p1 = true; d.j = pr + G; d.r = rr; }
       else { d.p1 = false; d.j = pr; d.r = rr - N1; }
     } else {
       const uint32_t q3 = q2 - (ns - G) * (N1 + N2);
@@ -630,7 +640,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   // T8_SCHED helpers -------------------------------------------------------------------
   auto decode = [&](uint32_t q, Slot& o) {
     if (q >= total) { o.q = T8_EXH; return; }
-    const ItemDec d = decode_item(q, ns, N1, N2, lag);
+    const ItemDec d = decode_item(q, ns, N1, N2, lag, args.p2_head);
     o.q = q; o.p1 = d.p1; o.j = d.j; o.r = d.r;
     const uint4 oi = args.order[d.j];
     o.loc = oi.x; o.base = oi.y; o.freeb = oi.z;
@@ -872,7 +882,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       o.q = T8_EXH;
       set_meta(sel, T8_EXH, false, 0);
       if (claim < total) {
-        const ItemDec d = decode_item(claim, ns, N1, N2, lag);
+        const ItemDec d = decode_item(claim, ns, N1, N2, lag, args.p2_head);
         o.p1 = d.p1; o.j = d.j; o.r = d.r;
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&o.loc)),
                      "l"(args.order + d.j) : "memory");

@@ -273,6 +273,7 @@ struct SlabArgs {
   void* ring;                // slab8_kernel<uint64_t, M, 2>: T8_RING slab buffers for pass-1 tiles
   int keep_policy;           // L2 policy of the pass-1 tile stores (0 evict_last, 1 evict_normal, 2 unchanged)
   int p2_prefetch;           // pass-2 items bulk-prefetch their columns into L2 (0 / 1)
+  uint32_t p2_head;          // decode_item: pass-1 items before the interleave (0xffffffff: none)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {

@@ -483,7 +483,8 @@ def test_slab_ring_lag_clamped():
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("env", [{"HC_SLAB_LAG": "2"}, {"HC_ENGINE": "slabx"}, {"HC_ENGINE": "slabx", "HC_SLABX_LAG": "1"}])
+@pytest.mark.parametrize("env", [{"HC_SLAB_LAG": "2"}, {"HC_ENGINE": "slabx"}, {"HC_ENGINE": "slabx", "HC_SLABX_LAG": "1"},
+                                 {"HC_P2_HEAD": "243"}, {"HC_KEEP_POLICY": "1", "HC_P2_PREFETCH": "1"}])
 def test_engine_variants_by_env(env):
     # engine knobs are environment variables read once per process: run them in a child
     # process against the oracle
