@@ -66,7 +66,9 @@ typedef struct hc_plan_s* hc_plan_t;
 /* Status text (static string). */
 const char* hc_status_str(hc_status s);
 
-/* 2^D and 3^D (0 if D is out of range). */
+/* 2^D and 3^D (0 if D is out of range, i.e. outside [1, HC_MAX_D]): the lengths of the
+ * inputs x, y in {0,1}^D and of the output z in {0,1,2}^D of the convolution
+ * z[k] = sum_{i+j=k} x[i] y[j] (PAPER.md 30-34, Introduction; reading R2 for D >= 1). */
 uint64_t hc_in_len(int D);
 uint64_t hc_out_len(int D);
 
@@ -77,7 +79,10 @@ uint64_t hc_out_len(int D);
 hc_status hc_plan_create(hc_plan_t* out, int D, hc_dtype dtype, int ngpu, int rank);
 hc_status hc_plan_destroy(hc_plan_t plan);
 
-/* Flat range [z_begin, z_end) of z owned by `rank` under the plan's ngpu-way split. */
+/* Flat range [z_begin, z_end) of z owned by `rank` under the plan's ngpu-way split: whole
+ * output slabs (fixed top trits t_T), which the paper's 4-way split computes independently
+ * of each other (PAPER.md 166-177, Methods), cut at equal estimated cost (hc_shard_range).
+ * Errors: HC_ERR_NULL (null pointer), HC_ERR_SHARD (rank outside [0, ngpu)). */
 hc_status hc_shard_info(hc_plan_t plan, int rank, uint64_t* z_begin, uint64_t* z_end);
 
 /* Pure host function (no device needed): the flat range [z_begin, z_end) of z that rank
@@ -95,7 +100,12 @@ hc_status hc_convolve(hc_plan_t plan, const void* x, const void* y, void* z, voi
 hc_status hc_convolve_sharded(hc_plan_t plan, const void* x, const void* y, void* z_shard,
                               void* stream);
 
-/* B independent convolutions of dimension D (row-major batches, device pointers). */
+/* B independent convolutions of dimension D (PAPER.md 30-34 for each pair; BASELINE.json
+ * config 2 / north_star (5): many small cubes).  Layout (reading R8): x, y are [B][2^D]
+ * row-major, z is [B][3^D] row-major; device pointers owned by the caller; x, y 16-byte
+ * aligned, z 8-byte aligned; z must not alias x or y.  Stream-ordered; int64 is exact mod
+ * 2^64 (reading R3).  Errors: HC_ERR_INVALID_DIM (B < 1 or D outside [1, HC_MAX_D]),
+ * HC_ERR_DTYPE, HC_ERR_NULL, HC_ERR_ALIGN, HC_ERR_DEVICE, HC_ERR_CUDA (launch failure). */
 hc_status hc_convolve_batched(int B, int D, hc_dtype dtype, const void* x, const void* y,
                               void* z, void* stream);
 
