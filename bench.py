@@ -115,7 +115,10 @@ def load_traffic(key):
 INT32_PEAK = 148 * 128 * 1.965e9
 
 
-def int_ops_per_output(D, k_top, interp_axes):
+def int_ops_per_output(D, k_top, interp_axes, narrow=False):
+    if narrow:  # batched D = 8 in the 32-bit ring (hc_tile8n.cuh): one instruction per add / mad
+        pair = (243 * (27 + 38) + 81 * 16 + 96 * 19 + 32 * 8) / 6561.0
+        return pair + (2.0 / 3.0) * interp_axes + 1.0  # + the sign extension of each output
     pair = (243 * (27 * 5 + 38 * 2) + 81 * 16 * 2 + 96 * 19 * 2 + 32 * 8 * 2) / 6561.0
     return pair * (4.0 / 3.0) ** k_top + (4.0 / 3.0) * interp_axes
 
@@ -546,7 +549,8 @@ def main():
               "peak": fp64_peak / 1e12, "unit": "T fp64 instr-lanes/s",
               "frac": (ops / (k_avg / 1e3) / fp64_peak) if k_avg else None}
     elif tdt == torch.int64 and w.get("app") != "conv1d":
-        ops_per_out = int_ops_per_output(Dk, ktop_k, interp_k)
+        narrow = batched and D == 8 and os.environ.get("HC_NARROW", "1") != "0"
+        ops_per_out = int_ops_per_output(Dk, ktop_k, interp_k, narrow)
         ops = ops_per_out * outs_per_launch
         co = {"bound": "int", "ops_per_output": ops_per_out,
               "achieved": ops / (k_avg / 1e3) / 1e12 if k_avg else None, "peak": INT32_PEAK / 1e12,

@@ -19,6 +19,7 @@
 #include "hc_tile.cuh"
 #include "hc_slab.cuh"
 #include "hc_slabx.cuh"
+#include "hc_tile8n.cuh"
 
 using namespace hc;
 
@@ -171,6 +172,87 @@ cudaError_t launch_tile8(const T* x, const T* y, T* z, int D, uint64_t slab0, ui
   LaunchScope ls("tile", st);
   kern<<<grid, T8_NT, T8Cfg<T>::SMEM, st>>>(x, y, z, D, slab0, nslab, nitems);
   return cudaGetLastError();
+}
+
+// batched D = 8 int64 in the 32-bit ring (hc_tile8n.cuh) + the 64-bit engine over the cubes
+// whose bound check failed.  The fallback list lives in stream-ordered scratch (B + 1 words),
+// so concurrent calls on different streams never share it.  HC_NARROW=0 disables the path.
+static bool use_narrow() {
+  static const bool on = [] {
+    const char* s = getenv("HC_NARROW");
+    return !(s && s[0] == '0');
+  }();
+  return on;
+}
+
+// the library's own stream-ordered pool on the current device: it keeps what it has mapped
+// (release threshold = max) so per-call scratch costs no remapping after the first call, and
+// it is separate from the process's default pool
+static cudaError_t scratch_pool(cudaMemPool_t& pool) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[kMaxDev] = {};
+  int d = 0;
+  cudaError_t e = cudaGetDevice(&d);
+  if (e != cudaSuccess) return e;
+  if (d < 0 || d >= kMaxDev) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> g(mu);
+  if (!pools[d]) {
+    cudaMemPoolProps pr = {};
+    pr.allocType = cudaMemAllocationTypePinned;
+    pr.location.type = cudaMemLocationTypeDevice;
+    pr.location.id = d;
+    e = cudaMemPoolCreate(&pools[d], &pr);
+    if (e != cudaSuccess) return e;
+    uint64_t keep = ~0ull;
+    e = cudaMemPoolSetAttribute(pools[d], cudaMemPoolAttrReleaseThreshold, &keep);
+    if (e != cudaSuccess) return e;
+  }
+  pool = pools[d];
+  return cudaSuccess;
+}
+
+static cudaError_t launch_tile8n(const uint64_t* x, const uint64_t* y, uint64_t* z, uint64_t B, cudaStream_t st) {
+  if (B >= (1ull << 32)) return cudaErrorInvalidValue;  // list entries are 32-bit cube indices
+  static int gn_cache[kMaxDev] = {}, gl_cache[kMaxDev] = {};
+  int gn_scratch = 0, gl_scratch = 0;
+  int& gn = dev_slot(gn_cache, gn_scratch);
+  int& gl = dev_slot(gl_cache, gl_scratch);
+  cudaError_t e;
+  if (!gn) {
+    auto kn = tile8n_kernel<8>;
+    e = cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T8N_SMEM);
+    if (e != cudaSuccess) return e;
+    int occ = 0, dev = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kn, T8_NT, T8N_SMEM);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    gn = occ * sms;
+  }
+  e = t8_grid(tile8_list_kernel, gl);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool;
+  e = scratch_pool(pool);
+  if (e != cudaSuccess) return e;
+  uint32_t* ws = nullptr;
+  e = cudaMallocFromPoolAsync((void**)&ws, sizeof(uint32_t) * (size_t)(B + 1), pool, st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(ws, 0, sizeof(uint32_t), st);
+  if (e == cudaSuccess) {
+    const unsigned grid = (unsigned)(B < (uint64_t)gn ? B : (uint64_t)gn);
+    LaunchScope ls("tile", st);
+    tile8n_kernel<8><<<grid, T8_NT, T8N_SMEM, st>>>(x, y, z, B, ws, ws + 1);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {  // exits at once when every cube was safe
+    const unsigned grid = (unsigned)(B < (uint64_t)gl ? B : (uint64_t)gl);
+    LaunchScope ls("tile_fb", st);
+    tile8_list_kernel<<<grid, T8_NT, T8Cfg<uint64_t>::SMEM, st>>>(x, y, z, ws, ws + 1);
+    e = cudaGetLastError();
+  }
+  cudaError_t ef = cudaFreeAsync(ws, st);
+  return e != cudaSuccess ? e : ef;
 }
 
 template <class T, int M>
@@ -689,7 +771,11 @@ extern "C" hc_status hc_convolve_batched(int B, int D, hc_dtype dtype, const voi
   const int L = D < kTileL ? D : kTileL;
   const uint64_t nslab = upow3(D - L);
   const uint64_t nitems = (uint64_t)B * nslab;
-  cudaError_t e = launch_any(dtype, x, y, z, D, 0, nslab, nitems, (cudaStream_t)stream);
+  cudaError_t e;
+  if (dtype == HC_INT64 && D == 8 && use_narrow())
+    e = launch_tile8n((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)z, (uint64_t)B, (cudaStream_t)stream);
+  else
+    e = launch_any(dtype, x, y, z, D, 0, nslab, nitems, (cudaStream_t)stream);
   return e == cudaSuccess ? HC_OK : HC_ERR_CUDA;
 }
 

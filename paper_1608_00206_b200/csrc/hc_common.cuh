@@ -6,7 +6,7 @@
 // result (c0, c1, c2) is interpolated back as (c0, (c1 - c0) - c2, c2) (t - z[0] - z[2],
 // lines 187-189; subtraction order of Algorithm 2's two loops, lines 248-251).
 //
-// Element arithmetic: uint64 (int64 as wrap-around, exact mod 2^64) or double.
+// Element arithmetic: uint64 (int64 as wrap-around, exact mod 2^64), uint32 (mod 2^32) or double.
 // This file shares nothing with oracle/ (test infrastructure).
 #pragma once
 #include <cstdint>
@@ -23,6 +23,12 @@ template <> struct Ar<uint64_t> {
   static __device__ __forceinline__ uint64_t sub(uint64_t a, uint64_t b) { return a - b; }
   // c + a*b (mod 2^64)
   static __device__ __forceinline__ uint64_t mad(uint64_t a, uint64_t b, uint64_t c) { return c + a * b; }
+};
+// the 32-bit ring (hc_tile8n.cuh: exact residues of int64 results that fit in 32 bits)
+template <> struct Ar<uint32_t> {
+  static __device__ __forceinline__ uint32_t add(uint32_t a, uint32_t b) { return a + b; }
+  static __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) { return a - b; }
+  static __device__ __forceinline__ uint32_t mad(uint32_t a, uint32_t b, uint32_t c) { return c + a * b; }
 };
 template <> struct Ar<double> {
   static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }

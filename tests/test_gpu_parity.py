@@ -92,6 +92,45 @@ def test_config_c2_batched_d8_full(hc, orc):
     assert np.array_equal(z.cpu().numpy(), orc.conv_batched(x, y))
 
 
+@pytest.mark.parametrize("B", [1, 7, 1500])
+def test_batched_d8_narrow_ring_boundary(hc, orc, B):
+    # batched D = 8 int64 runs in the 32-bit ring when 2^8 max|x| max|y| < 2^31 (every output is
+    # a sum of at most 2^8 products, PAPER.md 166-171; ring homomorphism, R3) and in
+    # the 64-bit engine otherwise.  Cubes straddle the bound: constant cubes x = a, y = b put
+    # 2^8 a b at the all-1 cell, so a b = 2^23 - 1 is the largest safe product (z = 2^31 - 256)
+    # and a b = 2^23 the first unsafe one (z = 2^31 needs 64 bits); signs flip the extremes to
+    # -2^31 + 256 and -2^31; random cubes mix safe small entries with full-range ones.
+    rng = np.random.default_rng(880 + B)
+    xb = np.empty((B, 256), dtype=np.int64)
+    yb = np.empty((B, 256), dtype=np.int64)
+    kinds = rng.integers(0, 6, B)
+    for i, k in enumerate(kinds):
+        if k == 0:   # largest safe constant cube
+            xb[i], yb[i] = 8191, 1025          # 8191 * 1025 = 2^23 - 1
+        elif k == 1:  # smallest unsafe constant cube
+            xb[i], yb[i] = -2048, 4096          # 2^23, negative: z = -2^31 at the all-1 cell
+        elif k == 2:
+            xb[i] = rng.integers(-255, 256, 256)
+            yb[i] = rng.integers(-255, 256, 256)
+        elif k == 3:  # one outlier entry makes the cube unsafe
+            xb[i] = rng.integers(0, 256, 256)
+            yb[i] = rng.integers(0, 256, 256)
+            yb[i, rng.integers(0, 256)] = 1 << 40
+        elif k == 4:
+            xb[i] = hcgen.splitmix64(9000 + i, 0, 256).view(np.int64)
+            yb[i] = hcgen.splitmix64(9000 + i, 1, 256).view(np.int64)
+        else:         # INT64_MIN: |x| = 2^63 must not wrap to a small magnitude
+            xb[i] = 0
+            xb[i, 5] = np.iinfo(np.int64).min
+            yb[i] = 1
+    if B == 1:
+        xb[0], yb[0] = 8191, -1025
+    z = torch.empty((B, 3 ** 8), dtype=torch.int64, device="cuda")
+    hc.convolve_batched(_gpu(xb), _gpu(yb), z)
+    torch.cuda.synchronize()
+    assert np.array_equal(z.cpu().numpy(), orc.conv_batched(xb, yb))
+
+
 def test_config_c3_d16_int64_full(hc, orc):
     x, y = hcgen.config_inputs("c3_d16_i64")
     got = _run(hc, x, y).cpu().numpy()
@@ -484,7 +523,8 @@ def test_slab_ring_lag_clamped():
 
 
 @pytest.mark.parametrize("env", [{"HC_SLAB_LAG": "2"}, {"HC_ENGINE": "slabx"}, {"HC_ENGINE": "slabx", "HC_SLABX_LAG": "1"},
-                                 {"HC_P2_HEAD": "243"}, {"HC_KEEP_POLICY": "1", "HC_P2_PREFETCH": "1"}])
+                                 {"HC_P2_HEAD": "243"}, {"HC_KEEP_POLICY": "1", "HC_P2_PREFETCH": "1"},
+                                 {"HC_NARROW": "0"}])
 def test_engine_variants_by_env(env):
     # engine knobs are environment variables read once per process: run them in a child
     # process against the oracle
