@@ -499,10 +499,12 @@ def main():
     peak, peak_src = load_peaks()
     evalpoint = args.variant in ("evalpoint", "evalpoint-peer") and "app" not in w and not batched
     if evalpoint:
-        # the dominant launches are the per-point (D-k)-dimensional convolutions (slab engine)
+        # the dominant launch is the batch of the rank's (D-k)-dimensional convolutions, one per
+        # owned evaluation point (slab engine over points x slabs)
         Dl = D - args.ep_k
-        outs_per_launch = 3 ** Dl
-        alg_bytes_per_launch = float((3 ** Dl + 2 * 2 ** Dl) * 8)
+        npts = (ep.e1 - ep.e0) / lps
+        outs_per_launch = npts * 3 ** Dl
+        alg_bytes_per_launch = float(npts * (3 ** Dl + 2 * 2 ** Dl) * 8)
     else:
         outs_per_launch = n_local / lps
         alg_bytes_per_launch = (n_local * 8 + in_bytes * lps) / lps

@@ -256,9 +256,10 @@ static cudaError_t launch_tile8n(const uint64_t* x, const uint64_t* y, uint64_t*
 }
 
 template <class T, int M>
-cudaError_t launch_prep(const T* x, const T* y, T* xu, T* yu, int k, cudaStream_t st) {
+cudaError_t launch_prep(const T* x, const T* y, T* xu, T* yu, int k, cudaStream_t st, unsigned batch = 1) {
+  // a batch of same-D problems stored back to back is one problem with batch * 2^k input slices
   LaunchScope lp("prep", st);
-  dim3 pg((unsigned)upow3(M), 1u << k, 2);
+  dim3 pg((unsigned)upow3(M), batch << k, 2);
   prep_kernel<T, M><<<pg, 256, 0, st>>>(x, y, xu, yu);
   return cudaGetLastError();
 }
@@ -313,7 +314,7 @@ cudaError_t launch_slabx_m(const T* x, const T* y, T* z, T* xu, T* yu, const Sla
     if (e != cudaSuccess) return e;
   }
   static const int lag_env = getenv("HC_SLABX_LAG") ? atoi(getenv("HC_SLABX_LAG")) : 3;
-  SlabxArgs sa{a.nslab, (uint32_t)(lag_env < 1 ? 1 : lag_env), a.ctr, a.order};
+  SlabxArgs sa{a.nslab, (uint32_t)(lag_env < 1 ? 1 : lag_env), a.ctr, a.order, a.bstride};
   LaunchScope ls("slab", st);
   kern<<<grid, SX_NT, SXCfg<T, M>::SMEM, st>>>(xu, yu, z, sa);
   return cudaGetLastError();
@@ -874,9 +875,15 @@ struct hc_ep_s {
   int D, k, ngpu, rank;
   hc_dtype dtype;
   uint64_t e0, e1, c0, c1;   // owned evaluation points and columns
-  hc_plan_t low = nullptr;   // plan of the (D-k)-dimensional convolution
-  void* xh = nullptr;        // forward-evaluated operands of one point (2^(D-k) each)
+  hc_plan_t low = nullptr;   // plan of the (D-k)-dimensional convolution (geometry; non-batched path)
+  void* xh = nullptr;        // forward-evaluated operands of the owned points ([point][2^(D-k)])
   void* yh = nullptr;
+  // batched two-level engine over all owned points (D - k >= 13): middle-axes tables of every
+  // point, the slab order of points x slabs, and the engine's counters
+  void* xu = nullptr;
+  void* yu = nullptr;
+  uint4* order = nullptr;
+  uint32_t* ctr = nullptr;
 };
 
 extern "C" hc_status hc_ep_range(int D, int k, int ngpu, int rank, uint64_t* e_begin, uint64_t* e_end,
@@ -900,11 +907,47 @@ extern "C" hc_status hc_ep_create(hc_ep_t* out, int D, int k, hc_dtype dtype, in
   p->D = D; p->k = k; p->ngpu = ngpu; p->rank = rank; p->dtype = dtype;
   hc_status s = hc_ep_range(D, k, ngpu, rank, &p->e0, &p->e1, &p->c0, &p->c1);
   if (s == HC_OK) s = hc_plan_create(&p->low, D - k, dtype, 1, 0);
-  if (s == HC_OK) {
-    const size_t bytes = sizeof(double) * (1ull << (D - k));
+  const uint64_t P = p->e1 - p->e0;
+  if (s == HC_OK && P > 0) {
+    const size_t bytes = sizeof(double) * (1ull << (D - k)) * P;
     if (cudaMalloc(&p->xh, bytes) != cudaSuccess || cudaMalloc(&p->yh, bytes) != cudaSuccess) {
       cudaGetLastError();
       s = HC_ERR_CAPACITY;
+    }
+  }
+  if (s == HC_OK && P > 0 && p->low->g.two_level) {
+    const Geometry& g = p->low->g;
+    const size_t tbl = sizeof(double) * (size_t)(1ull << g.k) * upow3(g.M) * 256 * P;
+    const uint64_t ns = P * g.nunits;  // slabs of all owned points
+    if (cudaMalloc(&p->xu, tbl) != cudaSuccess || cudaMalloc(&p->yu, tbl) != cudaSuccess ||
+        cudaMalloc(&p->ctr, sizeof(uint32_t) * (1 + 2 * ns)) != cudaSuccess ||
+        cudaMalloc(&p->order, sizeof(uint4) * ns) != cudaSuccess) {
+      cudaGetLastError();
+      s = HC_ERR_CAPACITY;
+    } else {
+      // processing order: every point's slabs, cost-sorted together (as slab_order), slab
+      // (point b, top index t) at output offset b * 3^k + t, problem index b in .w
+      std::vector<std::pair<int, uint64_t>> v(ns);
+      for (uint64_t i = 0; i < ns; ++i) {
+        uint64_t t = i % g.nunits;
+        int ones = 0;
+        for (int a = 0; a < g.k; ++a, t /= 3) ones += (t % 3 == 1);
+        v[i] = {ones, i};
+      }
+      std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      std::vector<uint4> h(ns);
+      for (uint64_t i = 0; i < ns; ++i) {
+        const uint64_t slab = v[i].second, b = slab / g.nunits;
+        uint64_t t = slab % g.nunits;
+        uint32_t base = 0, freeb = 0;
+        for (int a = 0; a < g.k; ++a, t /= 3) {
+          if (t % 3 == 2) base |= 1u << a;
+          else if (t % 3 == 1) freeb |= 1u << a;
+        }
+        h[i] = make_uint4((uint32_t)slab, base, freeb, (uint32_t)b);
+      }
+      if (cudaMemcpy(p->order, h.data(), sizeof(uint4) * ns, cudaMemcpyHostToDevice) != cudaSuccess)
+        s = HC_ERR_CUDA;
     }
   }
   if (s != HC_OK) {
@@ -920,32 +963,42 @@ extern "C" hc_status hc_ep_destroy(hc_ep_t p) {
   if (p->low) hc_plan_destroy(p->low);
   cudaFree(p->xh);
   cudaFree(p->yh);
+  cudaFree(p->xu);
+  cudaFree(p->yu);
+  cudaFree(p->order);
+  cudaFree(p->ctr);
   delete p;
   return HC_OK;
 }
 
 namespace {
+// all owned points in one pass: one evaluation launch for every point, then ONE batched
+// (D-k)-dimensional convolution over the points (the tile engine's batch for D - k <= 12, the
+// two-level engine over points x slabs otherwise), w = [point][3^(D-k)]
 template <class T>
 cudaError_t ep_local_t(hc_ep_t p, const T* x, const T* y, T* w, cudaStream_t st) {
   const int L = p->D - p->k;
-  const uint64_t nout = upow3(L);
-  for (uint64_t e = p->e0; e < p->e1; ++e) {
-    uint32_t base = 0, freeb = 0;
-    uint64_t t = e;
-    for (int a = 0; a < p->k; ++a, t /= 3) {
-      if (t % 3 == 2) base |= 1u << a;
-      else if (t % 3 == 1) freeb |= 1u << a;
-    }
-    {
-      LaunchScope ls("ep_eval", st);
-      dim3 g((unsigned)(((1ull << L) + 255) / 256), 2);
-      ep_eval_kernel<T><<<g, 256, 0, st>>>(x, y, (T*)p->xh, (T*)p->yh, L, base, freeb);
-      cudaError_t err = cudaGetLastError();
-      if (err != cudaSuccess) return err;
-    }
-    if (hc_convolve(p->low, p->xh, p->yh, w + (e - p->e0) * nout, st) != HC_OK) return cudaErrorLaunchFailure;
+  const uint64_t P = p->e1 - p->e0;
+  if (P == 0) return cudaSuccess;
+  {
+    LaunchScope ls("ep_eval", st);
+    dim3 g((unsigned)(((1ull << L) + 255) / 256), 2, (unsigned)P);
+    ep_eval_kernel<T><<<g, 256, 0, st>>>(x, y, (T*)p->xh, (T*)p->yh, L, p->k, p->e0);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
   }
-  return cudaSuccess;
+  const Geometry& g = p->low->g;
+  if (!g.two_level)
+    return launch_any(p->dtype, p->xh, p->yh, w, L, 0, g.nunits, P * g.nunits, st);
+  const uint64_t ns = P * g.nunits;
+  cudaError_t e = cudaErrorInvalidValue;
+  if (g.M == 5) e = launch_prep<T, 5>((const T*)p->xh, (const T*)p->yh, (T*)p->xu, (T*)p->yu, g.k, st, (unsigned)P);
+  if (g.M == 6) e = launch_prep<T, 6>((const T*)p->xh, (const T*)p->yh, (T*)p->xu, (T*)p->yu, g.k, st, (unsigned)P);
+  if (e != cudaSuccess) return e;
+  static const int lag = getenv("HC_SLAB_LAG") ? atoi(getenv("HC_SLAB_LAG")) : 1;
+  SlabArgs a{0, (uint32_t)ns, g.k, p->ctr, p->order, 0, (uint32_t)(lag < 1 ? 1 : lag), nullptr, nullptr, 0, 0,
+             0xffffffffu, (uint64_t)(1ull << g.k) * upow3(g.M) * 256};
+  return launch_slab8<T>((const T*)p->xh, (const T*)p->yh, w, (T*)p->xu, (T*)p->yu, g.M, a, st, /*prep=*/false);
 }
 template <class T>
 cudaError_t ep_finish_t(hc_ep_t p, const T* wt, T* z, cudaStream_t st) {

@@ -3,8 +3,8 @@
 //
 // The top k axes use the paper's Karatsuba split (PAPER.md 185-192) across ranks:
 //   ep_eval_kernel   xh[e_T][i_L] = sum_{i_T ~ e_T} x[i_T][i_L]  (forward over the top axes,
-//                    (a0, a0 + a1, a1) per axis; subsets in ascending order)
-//   (the (D-k)-dimensional convolution of xh, yh runs on the slab / tile engines)
+//                    (a0, a0 + a1, a1) per axis; subsets in ascending order), all owned e_T
+//   (the (D-k)-dimensional convolutions of xh, yh run as ONE batch on the slab / tile engines)
 //   ep_top_inverse   z[k_T][col] = inverse over the top axes of w[.][col]
 //                    ((c0, (c1 - c0) - c2, c2) per axis, PAPER.md 187-189, 248-251)
 #pragma once
@@ -12,13 +12,21 @@
 
 namespace hc {
 
-// grid (ceil(2^L / 256), 2 operands), block 256: one evaluation point e_T of the top k axes
+// every owned point at once: grid (ceil(2^L / 256), 2 operands, points), point e = e0 +
+// blockIdx.z into xh/yh + blockIdx.z * 2^L (trit split of e as in ep_local: digit 2 -> base
+// bit, digit 1 -> free bit)
 template <class T>
 __global__ void __launch_bounds__(256) ep_eval_kernel(const T* __restrict__ x, const T* __restrict__ y,
-                                                      T* __restrict__ xh, T* __restrict__ yh, int L,
-                                                      uint32_t base, uint32_t freeb) {
+                                                      T* __restrict__ xh, T* __restrict__ yh, int L, int k,
+                                                      uint64_t e0) {
   const uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x;
   if (i >= (1ull << L)) return;
+  uint32_t base = 0, freeb = 0;
+  uint32_t t = (uint32_t)(e0 + blockIdx.z);
+  for (int a = 0; a < k; ++a, t /= 3) {
+    if (t % 3 == 2) base |= 1u << a;
+    else if (t % 3 == 1) freeb |= 1u << a;
+  }
   const T* src = (blockIdx.y ? y : x) + i;
   T acc = T(0);
   uint32_t s = 0;
@@ -26,7 +34,7 @@ __global__ void __launch_bounds__(256) ep_eval_kernel(const T* __restrict__ x, c
     acc = Ar<T>::add(acc, __ldg(src + ((uint64_t)(base | s) << L)));
     s = (s - freeb) & freeb;
   } while (s != 0);
-  (blockIdx.y ? yh : xh)[i] = acc;
+  (blockIdx.y ? yh : xh)[((uint64_t)blockIdx.z << L) + i] = acc;
 }
 
 // one thread per column: load the 3^K evaluation values (coalesced across threads),

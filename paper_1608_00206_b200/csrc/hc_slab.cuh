@@ -552,32 +552,30 @@ __device__ __forceinline__ void p2_carry_chunk(const T* __restrict__ zs, uint32_
     }
   __syncthreads();
   if ((int)threadIdx.x == sched) mid();
-  // round 2: task (e_lo, pos) interpolates the HI axes and sums its values by valHI(e_hi)
-  T b[NB];
-  const bool t2 = task >= 0 && task < NLO * P2W;
+  // round 2: task (e_lo, pos) interpolates the HI axes and sums its values by valHI(e_hi); bin
+  // vhi goes to the cell the task itself read for e_hi = vhi (row vhi of its column), so no
+  // other thread's unread cell is overwritten and no barrier (nor live bins across one) is needed
+  static_assert(NB <= NHI && NB * P2S + 9 * NB * 15 <= T8Cfg<T>::ALIAS, "bins fit the exchange rows");
   const int el = task / P2W, pos = task - el * P2W;
-  if (t2) {
-    T v[NHI];
+  if (task >= 0 && task < NLO * P2W) {
+    T v[NHI], b[NB];
 #pragma unroll
     for (int e = 0; e < NHI; ++e) v[e] = sm[e * P2S + el * P2W + pos];
     static_assert(NB == (2 << HI) - 1, "bins of HI digits");
     inv_bin<HI, T>(v, b);
-  }
-  __syncthreads();  // the exchange is reused below
-  T* bs = sm;                    // [pos][vhi][e_lo]: 9 x NB x 27
-  T* cs = sm + 9 * NB * NLO;     // [pos][vhi][val3(e_lo)]: 9 x NB x 15
-  if (t2) {
 #pragma unroll
-    for (int i = 0; i < NB; ++i) bs[(pos * NB + i) * NLO + el] = b[i];
+    for (int i = 0; i < NB; ++i) sm[i * P2S + el * P2W + pos] = b[i];  // bs[vhi][e_lo][pos]
   }
+  T* cs = sm + NB * P2S;  // [pos][vhi][val3(e_lo)]: 9 x NB x 15, past the bin rows
   __syncthreads();
   // sum over e_lo by val3(e_lo): thread (pos, vhi)
   for (int t = threadIdx.x; t < 9 * NB; t += blockDim.x) {
+    const int tp = t / NB, tv = t - tp * NB;
     T cc[15];
 #pragma unroll
     for (int i = 0; i < 15; ++i) cc[i] = T(0);
 #pragma unroll
-    for (int e = 0; e < NLO; ++e) cc[bitval3<3>(e)] += bs[t * NLO + e];
+    for (int e = 0; e < NLO; ++e) cc[bitval3<3>(e)] += sm[tv * P2S + e * P2W + tp];
 #pragma unroll
     for (int i = 0; i < 15; ++i) cs[t * 15 + i] = cc[i];
   }
@@ -600,7 +598,8 @@ __device__ __forceinline__ void p2_carry_chunk(const T* __restrict__ zs, uint32_
 }
 
 struct __align__(16) Slot {
-  uint32_t loc, base, freeb, pad;  // = order[j] (16 B): slab offset; pass 1: trit split of its top index
+  uint32_t loc, base, freeb, pad;  // = order[j] (16 B): slab offset; pass 1: trit split of its top index;
+                                   // pad = problem index within a batch (SlabArgs::order)
   uint32_t q;                      // claim index, T8_EXH = past the end (or being decoded)
   uint32_t p1, j, r;
 };
@@ -643,7 +642,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
     const ItemDec d = decode_item(q, ns, N1, N2, lag, args.p2_head);
     o.q = q; o.p1 = d.p1; o.j = d.j; o.r = d.r;
     const uint4 oi = args.order[d.j];
-    o.loc = oi.x; o.base = oi.y; o.freeb = oi.z;
+    o.loc = oi.x; o.base = oi.y; o.freeb = oi.z; o.pad = oi.w;
   };
   // prefetch cursor: pass-1 slots in claim order (pf.pos = claim index of the cursor item)
   auto next = [&](Prefetch& c) -> bool {
@@ -657,8 +656,9 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
     if (best < 0) return false;
     const Slot& o = s_slot[best];
     c.pos = o.q;
-    c.sx0 = xu + (uint64_t)o.r * 256;
-    c.sy0 = yu + (uint64_t)o.r * 256;
+    const uint64_t off = (uint64_t)o.pad * args.bstride + (uint64_t)o.r * 256;  // problem o.pad of a batch
+    c.sx0 = xu + off;
+    c.sy0 = yu + off;
     c.stride = stride;
     c.base = o.base;
     c.freeb = o.freeb;
@@ -741,7 +741,8 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       if constexpr (EPI == 3) {
         if (p1 >= 0) {
           const uint32_t j1 = p1 == 0 ? jm.x : (p1 == 1 ? jm.y : jm.z);
-          p1_ready = j1 < T8_RING || (((cmask >> p1) & 1) && cv[p1] >= N2);
+          const uint32_t c1 = p1 == 0 ? cv[0] : (p1 == 1 ? cv[1] : cv[2]);  // no dynamic index: cv[] stays in registers
+          p1_ready = j1 < T8_RING || (((cmask >> p1) & 1) && c1 >= N2);
         }
       }
       sel = p2r >= 0 ? p2r : (p1_ready ? p1 : -1);

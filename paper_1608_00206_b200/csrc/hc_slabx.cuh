@@ -77,7 +77,8 @@ struct SlabxArgs {
   uint32_t nslab;      // slabs in this launch
   uint32_t lag;        // pass 1 of position j starts after pass 2 of position j - lag finished
   uint32_t* ctr;       // [0] pass-1 claims, [1] pass-2 claims, [2 + j] tiles done, [2 + ns + j] pass-2 done
-  const uint4* order;  // position j -> {slab offset, base, freeb, 0} (as SlabArgs::order)
+  const uint4* order;  // position j -> {slab offset, base, freeb, problem b} (as SlabArgs::order)
+  uint64_t bstride;    // elements between consecutive problems' middle-axes tables (batch)
 };
 
 // ---- small PTX wrappers ----------------------------------------------------------------
@@ -331,8 +332,8 @@ slabx_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
         ++qslot;
         if (!more) break;
         // the item's raw slices, pairs in ascending subsets of freeb (PAPER.md 173-177)
-        const T* sx0 = xu + (uint64_t)r * 256;
-        const T* sy0 = yu + (uint64_t)r * 256;
+        const T* sx0 = xu + (uint64_t)o.w * args.bstride + (uint64_t)r * 256;
+        const T* sy0 = yu + (uint64_t)o.w * args.bstride + (uint64_t)r * 256;
         const uint32_t base = o.y, freeb = o.z;
         uint32_t s = 0;
         do {

@@ -265,8 +265,10 @@ struct SlabArgs {
   uint32_t nslab;      // slabs in this launch
   int k;               // top axes
   uint32_t* ctr;       // [0] = work counter, [1 + j] = pass-1 tiles done in slab j
-  const uint4* order;  // processing position j -> {slab offset within the launch, base, freeb, 0}:
-                       // cost-sorted, with the trit split of the slab's top index precomputed
+  const uint4* order;  // processing position j -> {slab offset within the launch, base, freeb, problem b}:
+                       // cost-sorted, with the trit split of the slab's top index precomputed; b > 0
+                       // only for a batch of same-D problems (hc_ep_local), whose slabs are numbered
+                       // b * 3^k + t_T and whose middle-axes tables lie bstride elements apart
   int debug_skip;      // timing experiments only (HC_DEBUG_SKIP): 1 = no pass 2, 2 = no pass 1
   uint32_t lag;        // pass 2 of slab j is scheduled after pass 1 of slab j + lag (>= 1)
   unsigned long long* cout;  // slab8_kernel<uint64_t, M, 2>: carry bins (f1), else unused
@@ -274,6 +276,7 @@ struct SlabArgs {
   int keep_policy;           // L2 policy of the pass-1 tile stores (0 evict_last, 1 evict_normal, 2 unchanged)
   int p2_prefetch;           // pass-2 items bulk-prefetch their columns into L2 (0 / 1)
   uint32_t p2_head;          // decode_item: pass-1 items before the interleave (0xffffffff: none)
+  uint64_t bstride;          // elements between consecutive problems' middle-axes tables (batch)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {

@@ -319,7 +319,9 @@ def test_config_c5_d22_one_shard_of_eight(hc, orc):
 
 
 @pytest.mark.parametrize("D,k,dtype,nranks", [(11, 1, "int64", 2), (11, 2, "int64", 5), (12, 3, "int64", 3),
-                                              (12, 4, "int64", 8), (10, 2, "float64", 4), (14, 4, "int64", 1)])
+                                              (12, 4, "int64", 8), (10, 2, "float64", 4), (14, 4, "int64", 1),
+                                              # D - k >= 13: the points run as one batch on the two-level engine
+                                              (15, 2, "int64", 2), (16, 2, "float64", 3), (17, 4, "int64", 8)])
 def test_evalpoint_variant_emulated_ranks(hc, orc, D, k, dtype, nranks):
     # north_star (4): every rank's local step, the exchange emulated on one device (each rank's
     # columns gathered from all ranks' w), the top-axes interpolation; the 3^k strided chunks
@@ -365,6 +367,49 @@ def test_evalpoint_variant_emulated_ranks(hc, orc, D, k, dtype, nranks):
         p.finish(wt, z)
         torch.cuda.synchronize()
         _assert_close(z.cpu().numpy(), want, x, y)
+
+
+@pytest.mark.parametrize("D,k,nranks", [(17, 2, 2), (18, 3, 4)])
+def test_evalpoint_batched_slab_points_sampled(hc, orc, D, k, nranks):
+    # D - k = 15: each point is a two-level convolution with k' = 1 direct top axis (3 slabs), and
+    # all of a rank's points run as one batch of points x slabs through the slab engine; the
+    # evaluation-domain result of point e is checked against the (D-k)-dimensional oracle
+    # convolution of the point's evaluated inputs (forward over the top axes, PAPER.md 186-189),
+    # and the finished output on sampled cells against Algorithm 1
+    x, y = hcgen.make_pair(D, "int64", "uniform", 5100 + D, -500, 500)
+    L, nc, npnt = D - k, 3 ** (D - k), 3 ** k
+    xs, ys = _gpu(x), _gpu(y)
+    plans = [hc.EPPlan(D, k, "int64", nranks, r) for r in range(nranks)]
+    W = torch.empty((npnt, nc), dtype=torch.int64, device="cuda")
+    for p in plans:
+        w = torch.empty((p.e1 - p.e0) * nc, dtype=torch.int64, device="cuda")
+        p.local(xs, ys, w)
+        W[p.e0:p.e1] = w.view(-1, nc)
+    torch.cuda.synchronize()
+    xr, yr = x.reshape(2 ** k, 2 ** L), y.reshape(2 ** k, 2 ** L)
+    for e in (0, 1, npnt // 2 + 1, npnt - 1):   # points owned by different ranks
+        t, base, free = e, 0, 0
+        for a in range(k):
+            base |= (1 << a) if t % 3 == 2 else 0
+            free |= (1 << a) if t % 3 == 1 else 0
+            t //= 3
+        subs = [s for s in range(2 ** k) if s & ~free == 0]
+        xe = sum(xr[base | s] for s in subs)
+        ye = sum(yr[base | s] for s in subs)
+        ks = np.random.default_rng(e).integers(0, nc, 4000).astype(np.uint64)
+        assert np.array_equal(W[e].cpu().numpy()[ks.astype(np.int64)], orc.conv_cells(xe, ye, ks)), e
+    ks = np.random.default_rng(D).integers(0, 3 ** D, 20000)
+    got = np.empty(ks.size, dtype=np.int64)
+    for p in plans:
+        wt = W[:, p.c0:p.c1].contiguous().view(-1)
+        z = torch.empty_like(wt)
+        p.finish(wt, z)
+        torch.cuda.synchronize()
+        zz = z.view(npnt, -1).cpu().numpy()
+        col, row = ks % nc, ks // nc
+        m = (col >= p.c0) & (col < p.c1)
+        got[m] = zz[row[m], col[m] - p.c0]
+    assert np.array_equal(got, orc.conv_cells(x, y, ks.astype(np.uint64)))
 
 
 def test_output_at_odd_element_offset(hc, orc):

@@ -15,7 +15,7 @@ run() {  # tag, bench args, kernel regex, launch skip, traffic key
 }
 run c4 "--workload c4_d20_f64" "slab8" 1 "c4_d20_f64|split|slab"
 cp /tmp/p_c4.ncu-rep gpurun_out/prof/c4.ncu-rep
-run c2 "--workload c2_b65536_d8_i64" "tile8" 1 "c2_b65536_d8_i64|split|tile"
+run c2 "--workload c2_b65536_d8_i64" "tile8n" 1 "c2_b65536_d8_i64|split|tile"
 run c3 "--workload c3_d16_i64" "slab8" 1 "c3_d16_i64|split|slab"
 run c5 "--workload c5_d22_f64" "slab8" 8 "c5_d22_f64|split|slab"
 run f1 "--workload f1_conv1d_d20_i64" "slab8" 1 "f1_conv1d_d20_i64|conv1d|slab"
