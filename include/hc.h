@@ -104,8 +104,13 @@ hc_status hc_convolve_sharded(hc_plan_t plan, const void* x, const void* y, void
  * config 2 / north_star (5): many small cubes).  Layout (reading R8): x, y are [B][2^D]
  * row-major, z is [B][3^D] row-major; device pointers owned by the caller; x, y 16-byte
  * aligned, z 8-byte aligned; z must not alias x or y.  Stream-ordered; int64 is exact mod
- * 2^64 (reading R3).  Errors: HC_ERR_INVALID_DIM (B < 1 or D outside [1, HC_MAX_D]),
- * HC_ERR_DTYPE, HC_ERR_NULL, HC_ERR_ALIGN, HC_ERR_DEVICE, HC_ERR_CUDA (launch failure). */
+ * 2^64 (reading R3).  int64 at D = 8 computes every cube with 2^8 max|x| max|y| < 2^31 in
+ * 32-bit words (exact: reading R14) and the others in 64-bit words; the list of the latter
+ * lives in stream-ordered scratch (B + 1 words from a library-owned memory pool, freed on
+ * the stream), so concurrent calls on different streams are independent (HC_NARROW=0 in
+ * the environment forces 64-bit words).  Errors: HC_ERR_INVALID_DIM (B < 1 or D outside
+ * [1, HC_MAX_D]), HC_ERR_DTYPE, HC_ERR_NULL, HC_ERR_ALIGN, HC_ERR_DEVICE, HC_ERR_CUDA
+ * (launch or scratch-allocation failure). */
 hc_status hc_convolve_batched(int B, int D, hc_dtype dtype, const void* x, const void* y,
                               void* z, void* stream);
 
@@ -136,11 +141,17 @@ typedef struct hc_ep_s* hc_ep_t;
  * Requires ngpu <= 3^k; HC_ERR_SHARD otherwise. */
 hc_status hc_ep_range(int D, int k, int ngpu, int rank, uint64_t* e_begin, uint64_t* e_end,
                       uint64_t* col_begin, uint64_t* col_end);
-/* Plan for one rank (owns the (D-k)-dimensional plan and 2 x 2^(D-k) elements of scratch). */
+/* Plan for one rank: the (D-k)-dimensional geometry, the evaluated operands of every owned
+ * point (2 x P x 2^(D-k) elements, P = e_end - e_begin) and, when D - k >= 13, the
+ * two-level engine's middle-axes tables, slab order and counters for all P points.
+ * HC_ERR_CAPACITY when device memory runs out (nothing is left allocated). */
 hc_status hc_ep_create(hc_ep_t* out, int D, int k, hc_dtype dtype, int ngpu, int rank);
 hc_status hc_ep_destroy(hc_ep_t p);
 /* Local step: x, y (2^D each, device, replicated); w (device) receives
- * (e_end - e_begin) x 3^(D-k) elements, row e_T - e_begin. */
+ * (e_end - e_begin) x 3^(D-k) elements, row e_T - e_begin.  All owned points run as one
+ * batch: one evaluation launch, then one batched (D-k)-dimensional convolution (tile engine
+ * for D - k <= 12, two-level engine over points x slabs otherwise).  Stream-ordered; the
+ * plan's scratch is reused, so calls on one plan must not overlap (one stream at a time). */
 hc_status hc_ep_local(hc_ep_t p, const void* x, const void* y, void* w, void* stream);
 /* Final step: wt = [3^k][ncols] gathered columns of w (device), z = [3^k][ncols] (device),
  * ncols = col_end - col_begin; z must not alias wt. */

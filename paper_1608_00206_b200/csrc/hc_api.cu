@@ -201,11 +201,16 @@ static cudaError_t scratch_pool(cudaMemPool_t& pool) {
     pr.allocType = cudaMemAllocationTypePinned;
     pr.location.type = cudaMemLocationTypeDevice;
     pr.location.id = d;
-    e = cudaMemPoolCreate(&pools[d], &pr);
+    cudaMemPool_t np = nullptr;
+    e = cudaMemPoolCreate(&np, &pr);
     if (e != cudaSuccess) return e;
     uint64_t keep = ~0ull;
-    e = cudaMemPoolSetAttribute(pools[d], cudaMemPoolAttrReleaseThreshold, &keep);
-    if (e != cudaSuccess) return e;
+    e = cudaMemPoolSetAttribute(np, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (e != cudaSuccess) {
+      cudaMemPoolDestroy(np);
+      return e;
+    }
+    pools[d] = np;
   }
   pool = pools[d];
   return cudaSuccess;
