@@ -223,12 +223,13 @@ static cudaError_t launch_tile8n(const uint64_t* x, const uint64_t* y, uint64_t*
   int& gn = dev_slot(gn_cache, gn_scratch);
   int& gl = dev_slot(gl_cache, gl_scratch);
   cudaError_t e;
+  auto kn = tile8n_kernel<8>;
+  const size_t smem = T8N_SMEM;
   if (!gn) {
-    auto kn = tile8n_kernel<8>;
-    e = cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T8N_SMEM);
+    e = cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0, dev = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kn, T8_NT, T8N_SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kn, T8_NT, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     cudaGetDevice(&dev);
@@ -247,7 +248,7 @@ static cudaError_t launch_tile8n(const uint64_t* x, const uint64_t* y, uint64_t*
   if (e == cudaSuccess) {
     const unsigned grid = (unsigned)(B < (uint64_t)gn ? B : (uint64_t)gn);
     LaunchScope ls("tile", st);
-    tile8n_kernel<8><<<grid, T8_NT, T8N_SMEM, st>>>(x, y, z, B, ws, ws + 1);
+    kn<<<grid, T8_NT, smem, st>>>(x, y, z, B, ws, ws + 1);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) {  // exits at once when every cube was safe

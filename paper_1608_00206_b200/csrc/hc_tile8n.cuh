@@ -22,6 +22,13 @@ namespace hc {
 // F1 stage of 32-bit words: op * PN_OP + b_a2 * PN_A2 + e_S * PN_ROW + b_C.  PN_ROW = 12 words:
 // the F2 lanes (consecutive e_S) read 16 B at a 48-B stride, conflict-free per quarter warp;
 // PN_A2 = 8, PN_OP = 16 (mod 32): the 32 F1 lanes (op, b_a2, b_C) store to 32 distinct banks.
+// The CTA's three store rounds are kept in step by barriers (0.688 vs 0.700 ms at config 2,
+// as for the 64-bit tile).  Measured and dropped: P and S in separate buffers with a 2-stage
+// raw ring, three barriers per cube instead of five (0.706 ms with the rounds in step, 0.726
+// without): the next cube's F1 then overlaps the stores, which costs more than the barriers.
+#ifndef HC_T8N_INSTEP
+#define HC_T8N_INSTEP 1
+#endif
 constexpr int PN_ROW = 12, PN_A2 = 1000, PN_OP = 2000, PN_SZ = 4000;
 constexpr int T8N_S = 6561;                           // tile exchange (32-bit words), aliases P
 constexpr int T8N_ALIAS = T8N_S > PN_SZ ? T8N_S : PN_SZ;
@@ -167,6 +174,9 @@ tile8n_kernel(const uint64_t* __restrict__ x, const uint64_t* __restrict__ y, ui
 #pragma unroll
           for (int e = 0; e < 9; ++e) st_cs_i64(zt + e * 729 + col, v[e]);
         }
+#if HC_T8N_INSTEP
+        if (r < 2) __syncthreads();  // the CTA's store rounds in step
+#endif
       }
     } else if (tid == 0) {
       fb_list[atomicAdd(fb_count, 1u)] = (uint32_t)cube;  // the 64-bit engine redoes this cube
