@@ -123,7 +123,7 @@ hc_status hc_convolve_host(hc_plan_t plan, const void* x_host, const void* y_hos
                            void* z_host, void* stream);
 
 /* ---- Evaluation-point variant of the multi-GPU split (BASELINE.json north_star (4);
- * SURVEY.md §8(e) "K5b").  The top k axes (1 <= k <= 4, k < D) use the paper's Karatsuba
+ * SURVEY.md §8(e) "K5b").  The top k axes (1 <= k <= 5, k < D) use the paper's Karatsuba
  * split (PAPER.md 185-192) ACROSS ranks: rank r owns the evaluation points
  * e_T in [e_begin, e_end) of {0,1,2}^k (flat base-3 index, trit b = axis D-k+b) and computes
  *     w[e_T][.] = conv_{D-k}( xh[e_T], yh[e_T] ),   xh[e_T][i_L] = sum_{i_T ~ e_T} x[i_T][i_L]

@@ -895,7 +895,7 @@ struct hc_ep_s {
 extern "C" hc_status hc_ep_range(int D, int k, int ngpu, int rank, uint64_t* e_begin, uint64_t* e_end,
                                  uint64_t* col_begin, uint64_t* col_end) {
   if (!e_begin || !e_end || !col_begin || !col_end) return HC_ERR_NULL;
-  if (D < 2 || D > HC_MAX_D || k < 1 || k > 4 || k >= D) return HC_ERR_INVALID_DIM;
+  if (D < 2 || D > HC_MAX_D || k < 1 || k > EP_MAX_K || k >= D) return HC_ERR_INVALID_DIM;
   const uint64_t np = upow3(k), nc = upow3(D - k);
   if (ngpu < 1 || rank < 0 || rank >= ngpu || (uint64_t)ngpu > np) return HC_ERR_SHARD;
   *e_begin = np * (uint64_t)rank / (uint64_t)ngpu;
@@ -1011,12 +1011,21 @@ cudaError_t ep_finish_t(hc_ep_t p, const T* wt, T* z, cudaStream_t st) {
   const uint64_t ncols = p->c1 - p->c0;
   if (ncols == 0) return cudaSuccess;
   const unsigned g = (unsigned)((ncols + 127) / 128);
+  if (p->k == 5) {
+    cudaError_t e = cudaFuncSetAttribute(ep_top_inverse5<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)EP5_SMEM);
+    if (e != cudaSuccess) return e;
+  }
   LaunchScope ls("ep_inverse", st);
   switch (p->k) {
     case 1: ep_top_inverse<T, 1><<<g, 128, 0, st>>>(wt, z, ncols); break;
     case 2: ep_top_inverse<T, 2><<<g, 128, 0, st>>>(wt, z, ncols); break;
     case 3: ep_top_inverse<T, 3><<<g, 128, 0, st>>>(wt, z, ncols); break;
-    default: ep_top_inverse<T, 4><<<g, 128, 0, st>>>(wt, z, ncols); break;
+    case 4: ep_top_inverse<T, 4><<<g, 128, 0, st>>>(wt, z, ncols); break;
+    default:
+      ep_top_inverse5<T, false><<<(unsigned)((ncols + EP5_CW - 1) / EP5_CW), 256, EP5_SMEM, st>>>(
+          wt, EPPeer{}, z, ncols, ncols, 0);
+      break;
   }
   return cudaGetLastError();
 }
@@ -1051,14 +1060,21 @@ extern "C" hc_status hc_ep_finish_peer(hc_ep_t p, const void* const* w_ranks, vo
   if (ncols == 0) return HC_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned g = (unsigned)((ncols + 127) / 128);
-  LaunchScope ls("ep_inverse_peer", st);
   auto go = [&](auto tag) {
     using T = decltype(tag);
+    if (p->k == 5 && cudaFuncSetAttribute(ep_top_inverse5<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)EP5_SMEM) != cudaSuccess)
+      return;
+    LaunchScope ls("ep_inverse_peer", st);
     switch (p->k) {
       case 1: ep_top_inverse_peer<T, 1><<<g, 128, 0, st>>>(pe, (T*)z, ncols, nct, p->c0); break;
       case 2: ep_top_inverse_peer<T, 2><<<g, 128, 0, st>>>(pe, (T*)z, ncols, nct, p->c0); break;
       case 3: ep_top_inverse_peer<T, 3><<<g, 128, 0, st>>>(pe, (T*)z, ncols, nct, p->c0); break;
-      default: ep_top_inverse_peer<T, 4><<<g, 128, 0, st>>>(pe, (T*)z, ncols, nct, p->c0); break;
+      case 4: ep_top_inverse_peer<T, 4><<<g, 128, 0, st>>>(pe, (T*)z, ncols, nct, p->c0); break;
+      default:
+        ep_top_inverse5<T, true><<<(unsigned)((ncols + EP5_CW - 1) / EP5_CW), 256, EP5_SMEM, st>>>(
+            nullptr, pe, (T*)z, ncols, nct, p->c0);
+        break;
     }
   };
   if (p->dtype == HC_INT64) go(uint64_t{});

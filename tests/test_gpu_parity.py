@@ -321,7 +321,9 @@ def test_config_c5_d22_one_shard_of_eight(hc, orc):
 @pytest.mark.parametrize("D,k,dtype,nranks", [(11, 1, "int64", 2), (11, 2, "int64", 5), (12, 3, "int64", 3),
                                               (12, 4, "int64", 8), (10, 2, "float64", 4), (14, 4, "int64", 1),
                                               # D - k >= 13: the points run as one batch on the two-level engine
-                                              (15, 2, "int64", 2), (16, 2, "float64", 3), (17, 4, "int64", 8)])
+                                              (15, 2, "int64", 2), (16, 2, "float64", 3), (17, 4, "int64", 8),
+                                              # k = 5: 243 points, interpolated in shared memory
+                                              (9, 5, "int64", 8), (13, 5, "float64", 3), (17, 5, "int64", 7)])
 def test_evalpoint_variant_emulated_ranks(hc, orc, D, k, dtype, nranks):
     # north_star (4): every rank's local step, the exchange emulated on one device (each rank's
     # columns gathered from all ranks' w), the top-axes interpolation; the 3^k strided chunks
@@ -369,7 +371,7 @@ def test_evalpoint_variant_emulated_ranks(hc, orc, D, k, dtype, nranks):
         _assert_close(z.cpu().numpy(), want, x, y)
 
 
-@pytest.mark.parametrize("D,k,nranks", [(17, 2, 2), (18, 3, 4)])
+@pytest.mark.parametrize("D,k,nranks", [(17, 2, 2), (18, 3, 4), (19, 5, 8)])
 def test_evalpoint_batched_slab_points_sampled(hc, orc, D, k, nranks):
     # D - k = 15: each point is a two-level convolution with k' = 1 direct top axis (3 slabs), and
     # all of a rank's points run as one batch of points x slabs through the slab engine; the

@@ -105,7 +105,7 @@ def test_shard_errors(hc):
         hc.shard_range(8, 2, 0)   # a single slab cannot be split
 
 
-@pytest.mark.parametrize("D,k", [(6, 1), (12, 3), (20, 4), (22, 4)])
+@pytest.mark.parametrize("D,k", [(6, 1), (12, 3), (20, 4), (22, 4), (20, 5)])
 def test_ep_ranges_partition(hc, D, k):
     # evaluation-point variant (hc_ep_range): points and columns are split contiguously,
     # disjointly, in rank order, sizes within one of each other
@@ -122,7 +122,7 @@ def test_ep_ranges_partition(hc, D, k):
     with pytest.raises(hc.HCError):
         hc.ep_range(D, k, 3 ** k + 1, 0)
     with pytest.raises(hc.HCError):
-        hc.ep_range(D, 5, 1, 0)
+        hc.ep_range(D, 6, 1, 0)   # k <= 5 (EP_MAX_K)
 
 
 def _build_example(tmp_path):
