@@ -270,16 +270,16 @@ cudaError_t launch_prep(const T* x, const T* y, T* xu, T* yu, int k, cudaStream_
   return cudaGetLastError();
 }
 
-template <class T, int M, int EPI = 0>
+template <class T, int M, int EPI = 0, int P2CH = T8_P2CH>
 cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st,
                            bool prep) {
-  auto kern = slab8_kernel<T, M, EPI>;
+  auto kern = slab8_kernel<T, M, EPI, P2CH>;
   static int gm_cache[kMaxDev] = {};
   int gm_scratch = 0;
   int& grid_max = dev_slot(gm_cache, gm_scratch);
   cudaError_t e = t8_grid(kern, grid_max);
   if (e != cudaSuccess) return e;
-  const uint64_t items = (uint64_t)a.nslab * (upow3(M) + upow3(8) / (P2W * T8_P2CH));
+  const uint64_t items = (uint64_t)a.nslab * (upow3(M) + upow3(8) / (P2W * P2CH));
   const unsigned grid = (unsigned)(items < (uint64_t)grid_max ? items : (uint64_t)grid_max);
   e = cudaMemsetAsync(a.ctr, 0, sizeof(uint32_t) * (1 + 2 * (size_t)a.nslab), st);
   if (e != cudaSuccess) return e;
@@ -355,6 +355,13 @@ cudaError_t launch_slab8(const T* x, const T* y, T* z, T* xu, T* yu, int M, cons
     switch (M) {
       case 5: return launch_slabx_m<T, 5>(x, y, z, xu, yu, a, st, prep);
       case 6: return launch_slabx_m<T, 6>(x, y, z, xu, yu, a, st, prep);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (a.nslab <= 3 && a.p2_head == 0xffffffffu) {  // few slabs: single-chunk pass-2 items
+    switch (M) {
+      case 5: return launch_slab8_m<T, 5, 0, 1>(x, y, z, xu, yu, a, st, prep);
+      case 6: return launch_slab8_m<T, 6, 0, 1>(x, y, z, xu, yu, a, st, prep);
       default: return cudaErrorInvalidValue;
     }
   }

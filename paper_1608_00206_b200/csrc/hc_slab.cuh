@@ -607,11 +607,13 @@ static_assert(T8_QN == 3, "the scheduler packs the slots' claim indices into one
 
 // EPI 2: carries fused into pass 2 (f1, uint64 only), tiles in place in z; EPI 3: the same
 // with the tiles in a ring of T8_RING slab buffers (no 3^D buffer)
-template <class T, int M, int EPI = 0>
+// P2CH: 9-column chunks per pass-2 item (T8_P2CH; 1 for launches of at most 3 slabs, where the
+// last slab's pass 2 would otherwise run on a third of the CTAs: D = 14 0.099 -> 0.070 ms)
+template <class T, int M, int EPI = 0, int P2CH = T8_P2CH>
 __global__ void __launch_bounds__(T8_NT, 2)
 slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__ z, SlabArgs args) {
   constexpr uint32_t N1 = (uint32_t)ipow3(M);
-  constexpr uint32_t N2 = (uint32_t)(ipow3(8) / (P2W * T8_P2CH));
+  constexpr uint32_t N2 = (uint32_t)(ipow3(8) / (P2W * P2CH));
   constexpr uint64_t SLAB = upow3(M + 8);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -837,9 +839,9 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
           for (int b = 0; b < args.k; ++b, t /= 3) vtop += (t % 3) << b;
         }
 #pragma unroll 1
-        for (int ch = 0; ch < T8_P2CH; ++ch) {
+        for (int ch = 0; ch < P2CH; ++ch) {
           if (ch) __syncthreads();  // the exchange buffer is rewritten by the next chunk
-          const uint32_t cc = it.r * T8_P2CH + ch;  // chunk = tile digits k2..k7
+          const uint32_t cc = it.r * P2CH + ch;  // chunk = tile digits k2..k7
           uint64_t vcol = 0;
           {
             uint32_t t = cc;
@@ -852,19 +854,19 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       if (args.p2_prefetch) {
         // pull the item's later chunks into L2 while chunk 0 runs: part of the slab may have been
         // evicted to HBM since pass 1 wrote it; one bulk L2 prefetch (TMA unit, no registers, no
-        // shared memory) per row of the item's P2W * T8_P2CH columns, 16-B aligned cover
+        // shared memory) per row of the item's P2W * P2CH columns, 16-B aligned cover
         constexpr int NROW = ipow3(M);
-        const uint64_t c0 = (uint64_t)it.r * (P2W * T8_P2CH);
+        const uint64_t c0 = (uint64_t)it.r * (P2W * P2CH);
         for (int row = threadIdx.x; row < NROW; row += T8_NT) {
           const uintptr_t a = reinterpret_cast<uintptr_t>(zs + (uint64_t)row * 6561ull + c0);
-          const uintptr_t lo = a & ~(uintptr_t)15, hi = (a + 8 * P2W * T8_P2CH + 15) & ~(uintptr_t)15;
+          const uintptr_t lo = a & ~(uintptr_t)15, hi = (a + 8 * P2W * P2CH + 15) & ~(uintptr_t)15;
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
         }
       }
 #pragma unroll 1
-      for (int ch = 0; ch < T8_P2CH; ++ch) {
+      for (int ch = 0; ch < P2CH; ++ch) {
         if (ch) __syncthreads();  // the exchange buffer is rewritten by the next chunk
-        p2_item<T, M, 8>(zs, it.r * T8_P2CH + ch, sm, threadIdx.x < 243 ? (int)threadIdx.x : -1,
+        p2_item<T, M, 8>(zs, it.r * P2CH + ch, sm, threadIdx.x < 243 ? (int)threadIdx.x : -1,
                          ch == 0 ? T8_SCHED : -1, signal, [] { __syncthreads(); });
       }
       }
