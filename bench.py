@@ -509,7 +509,7 @@ def main():
         outs_per_launch = n_local / lps
         alg_bytes_per_launch = (n_local * 8 + in_bytes * lps) / lps
     achieved = alg_bytes_per_launch / (k_avg / 1e3) / 1e9 if k_avg > 0 else None
-    tkey = f"{wl}|{w.get('app', args.variant)}|{prof_name}"
+    tkey = f"{wl}|{w.get('app', args.variant)}|{prof_name}" + ("|slabx" if os.environ.get("HC_ENGINE") == "slabx" else "")
     traffic, tsrc = load_traffic(tkey)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_source": tsrc,

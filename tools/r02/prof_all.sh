@@ -25,7 +25,8 @@ run f4 "--workload f4_difference_d20_f64" "slab8" 1 "f4_difference_d20_f64|diffe
 run ep "--workload c4_d20_f64 --variant evalpoint --ep-k 4" "slab8" 1 "c4_d20_f64|evalpoint|slab"
 run epinv "--workload c4_d20_f64 --variant evalpoint --ep-k 4" "ep_top_inverse" 1
 run c1 "--workload c1_d10_i64" "tile8" 1 "c1_d10_i64|split|tile"
-export HC_ENGINE=slabx; run sx "--workload c4_d20_f64" "slabx" 1; unset HC_ENGINE
+run epp "--workload c4_d20_f64 --variant evalpoint-peer --ep-k 4" "slab8" 1 "c4_d20_f64|evalpoint-peer|slab"
+export HC_ENGINE=slabx; run sx "--workload c4_d20_f64" "slabx" 1 "c4_d20_f64|split|slab|slabx"; unset HC_ENGINE
 $B --workload c4_d20_f64 > gpurun_out/prof/ll.plain 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_c4.csv $B --workload c4_d20_f64 > gpurun_out/prof/ll.log 2>&1
 echo "launch list rc=$?"
