@@ -131,6 +131,29 @@ def test_batched_d8_narrow_ring_boundary(hc, orc, B):
     assert np.array_equal(z.cpu().numpy(), orc.conv_batched(xb, yb))
 
 
+def test_batched_d8_concurrent_streams(hc, orc):
+    # the 32-bit path's fallback list is per-call stream-ordered scratch: two batches with
+    # different unsafe cubes, launched back to back on two streams, must not see each other's list
+    B = 600
+    xa, ya = hcgen.make_batched_fast(B, 8, 0, 255, 4101)
+    xb, yb = hcgen.make_batched_fast(B, 8, 0, 255, 4102)
+    xa[::7, 3] = 1 << 36     # every 7th cube of batch a needs 64-bit words
+    yb[5::11, 200] = -(1 << 35)
+    ga, gb = [(_gpu(x), _gpu(y)) for x, y in ((xa, ya), (xb, yb))]
+    za = torch.empty((B, 3 ** 8), dtype=torch.int64, device="cuda")
+    zb = torch.empty_like(za)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            hc.convolve_batched(ga[0], ga[1], za, stream=s1)
+        with torch.cuda.stream(s2):
+            hc.convolve_batched(gb[0], gb[1], zb, stream=s2)
+    torch.cuda.synchronize()
+    assert np.array_equal(za.cpu().numpy(), orc.conv_batched(xa, ya))
+    assert np.array_equal(zb.cpu().numpy(), orc.conv_batched(xb, yb))
+
+
 def test_config_c3_d16_int64_full(hc, orc):
     x, y = hcgen.config_inputs("c3_d16_i64")
     got = _run(hc, x, y).cpu().numpy()
