@@ -251,6 +251,42 @@ def test_host_entry_point(hc, orc):
         assert torch.equal(zh, zd.cpu())
 
 
+@pytest.mark.parametrize("D", [3, 8, 11, 13, 16])
+def test_delta_and_zero_inputs(hc, D):
+    # degenerate inputs against their closed forms (no oracle): x = delta_a, y = delta_b gives
+    # z = delta at T(a) + T(b) with T(i) = sum_b i_b 3^b (the carry-free sum, PAPER.md 359-365);
+    # zero inputs give zero everywhere -- z is pre-filled with garbage so every cell must be written
+    rng = np.random.default_rng(D)
+    T = lambda i: sum(((int(i) >> b) & 1) * 3 ** b for b in range(D))
+    for dtype, tdt in (("int64", torch.int64), ("float64", torch.float64)):
+        for a, b in ((0, 0), ((1 << D) - 1, (1 << D) - 1), tuple(int(v) for v in rng.integers(0, 1 << D, 2))):
+            x = np.zeros(1 << D, dtype=dtype)
+            y = np.zeros(1 << D, dtype=dtype)
+            x[a], y[b] = 3, -5
+            z = torch.full((3 ** D,), 7, dtype=tdt, device="cuda")
+            hc.Plan(D, dtype).convolve(_gpu(x), _gpu(y), z)
+            torch.cuda.synchronize()
+            want = np.zeros(3 ** D, dtype=dtype)
+            want[T(a) + T(b)] = -15
+            assert np.array_equal(z.cpu().numpy(), want), (dtype, a, b)
+        zero = np.zeros(1 << D, dtype=dtype)
+        z = torch.full((3 ** D,), 7, dtype=tdt, device="cuda")
+        hc.Plan(D, dtype).convolve(_gpu(zero), _gpu(zero), z)
+        torch.cuda.synchronize()
+        assert not torch.any(z != 0)
+    # batched (int64 D = 8: the 32-bit path), one delta cube and one zero cube
+    if D == 8:
+        xb = np.zeros((2, 256), dtype=np.int64)
+        yb = np.zeros((2, 256), dtype=np.int64)
+        xb[0, 200], yb[0, 77] = -4, 9
+        zb = torch.full((2, 3 ** 8), 7, dtype=torch.int64, device="cuda")
+        hc.convolve_batched(_gpu(xb), _gpu(yb), zb)
+        torch.cuda.synchronize()
+        want = np.zeros((2, 3 ** 8), dtype=np.int64)
+        want[0, T(200) + T(77)] = -36
+        assert np.array_equal(zb.cpu().numpy(), want)
+
+
 def test_commutativity_int64(hc):
     D = 11
     x, y = hcgen.make_pair(D, "int64", "uniform", 9, -5000, 5000)
