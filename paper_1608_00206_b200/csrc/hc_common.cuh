@@ -12,6 +12,25 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Bounds-checked development build (-DHC_CHECK, tools/build_variant.sh check -DHC_CHECK): logical
+// index invariants of every engine are asserted on the device (compute-sanitizer is not
+// available on this pool); the default build compiles them out.
+#ifdef HC_CHECK
+#include <cstdio>
+#define HC_ASSERT(c)                                                                                   \
+  do {                                                                                                 \
+    if (!(c)) {                                                                                        \
+      printf("HC_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                                        \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#else
+#define HC_ASSERT(c) \
+  do {               \
+  } while (0)
+#endif
+
 namespace hc {
 
 __host__ __device__ constexpr int ipow3(int n) { return n <= 0 ? 1 : 3 * ipow3(n - 1); }

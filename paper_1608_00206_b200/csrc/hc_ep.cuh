@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(256) ep_eval_kernel(const T* __restrict__ x, c
   if (i >= (1ull << L)) return;
   uint32_t base = 0, freeb = 0;
   uint32_t t = (uint32_t)(e0 + blockIdx.z);
+  HC_ASSERT(t < upow3(k));
   for (int a = 0; a < k; ++a, t /= 3) {
     if (t % 3 == 2) base |= 1u << a;
     else if (t % 3 == 1) freeb |= 1u << a;

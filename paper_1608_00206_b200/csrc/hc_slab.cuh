@@ -179,6 +179,7 @@ struct RawRing {
 };
 template <class T>
 __device__ __forceinline__ void t8_issue(RawRing& rr, const T* sx, const T* sy, T* R, uint64_t pol) {
+  HC_ASSERT(rr.seq - rr.done < (uint32_t)T8_NRAW);  // never overwrite a stage F1 has not read
   const uint32_t st = rr.seq % T8_NRAW;
   uint64_t* bar = &rr.bar[st];
   T* dst = R + st * RS_SZ;
@@ -275,6 +276,7 @@ __device__ __forceinline__ void pf_pump(Prefetch& pf, RawRing& rr, T* R, uint64_
       fenced = true;
     }
     const uint64_t iT = pf.base | pf.s, jT = pf.base | (pf.freeb & ~pf.s);
+    HC_ASSERT((pf.base & pf.freeb) == 0 && (pf.s & ~pf.freeb) == 0 && pf.left > 0);
     t8_issue<T>(rr, (const T*)pf.sx0 + iT * pf.stride, (const T*)pf.sy0 + jT * pf.stride, R, pol);
     pf.s = (pf.s - pf.freeb) & pf.freeb;
     --pf.left;
@@ -414,6 +416,7 @@ tile8_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z
   for (uint64_t w = blockIdx.x; w < nitems; w += gridDim.x) {
     const uint64_t b = w / nslab;
     uint32_t base, freeb;
+    HC_ASSERT(slab0 + (w - b * nslab) < upow3(k));
     trit_split(slab0 + (w - b * nslab), k, base, freeb);
     tile8<T, true>(1 << __popc(freeb), z + w * 6561ull, sm, rr, 0, pump, [] {});
     __syncthreads();  // S (aliases P) is free before the next tile's F1
@@ -539,6 +542,7 @@ __device__ __forceinline__ void p2_carry_chunk(const T* __restrict__ zs, uint32_
   constexpr int NU = 15 + 8 * (NB - 1);      // u = val3(e_lo) + 8 valHI in [0, NU)
   constexpr uint64_t ROW = 6561;
   const uint64_t col0 = (uint64_t)c * P2W;
+  HC_ASSERT(col0 + P2W <= ROW);
   // round 1: task (e_hi, pos) loads its 27 column entries, interpolates the LO axes
   if (task >= 0)
     for (int w = task; w < NHI * P2W; w += 243) {
@@ -642,6 +646,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   auto decode = [&](uint32_t q, Slot& o) {
     if (q >= total) { o.q = T8_EXH; return; }
     const ItemDec d = decode_item(q, ns, N1, N2, lag, args.p2_head);
+    HC_ASSERT(d.j < ns && d.r < (d.p1 ? N1 : N2));
     o.q = q; o.p1 = d.p1; o.j = d.j; o.r = d.r;
     const uint4 oi = args.order[d.j];
     o.loc = oi.x; o.base = oi.y; o.freeb = oi.z; o.pad = oi.w;
@@ -815,6 +820,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       }
     }
     PH_MARK(0);
+    HC_ASSERT(it.loc < ns && it.j < ns && it.r < (it.p1 ? N1 : N2) && (it.base & it.freeb) == 0);
     T* zs = EPI == 3 ? reinterpret_cast<T*>(args.ring) + (uint64_t)(it.j % T8_RING) * SLAB
                      : z + (uint64_t)it.loc * SLAB;
     if (it.p1) {
@@ -886,6 +892,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
       set_meta(sel, T8_EXH, false, 0);
       if (claim < total) {
         const ItemDec d = decode_item(claim, ns, N1, N2, lag, args.p2_head);
+        HC_ASSERT(d.j < ns && d.r < (d.p1 ? N1 : N2));
         o.p1 = d.p1; o.j = d.j; o.r = d.r;
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&o.loc)),
                      "l"(args.order + d.j) : "memory");

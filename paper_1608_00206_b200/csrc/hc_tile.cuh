@@ -320,6 +320,7 @@ __device__ __forceinline__ void p2_item(T* __restrict__ zs, uint32_t c, T* sm, i
   constexpr int LO = Q::LO, HI = Q::HI, NLO = Q::NLO, NHI = Q::NHI, P2S = Q::P2S;
   constexpr uint64_t ROW = upow3(L);
   const uint64_t col0 = (uint64_t)c * P2W;
+  HC_ASSERT(col0 + P2W <= ROW && task < 243);
   // round 1: task (e_hi, pos) loads its 3^LO column entries, interpolates over LO axes
   if (task >= 0)
     for (int w = task; w < NHI * P2W; w += 243) {

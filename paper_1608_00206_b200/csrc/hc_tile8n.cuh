@@ -179,7 +179,9 @@ tile8n_kernel(const uint64_t* __restrict__ x, const uint64_t* __restrict__ y, ui
 #endif
       }
     } else if (tid == 0) {
-      fb_list[atomicAdd(fb_count, 1u)] = (uint32_t)cube;  // the 64-bit engine redoes this cube
+      const uint32_t slot = atomicAdd(fb_count, 1u);
+      HC_ASSERT(slot < nitems);
+      fb_list[slot] = (uint32_t)cube;  // the 64-bit engine redoes this cube
     }
     __syncthreads();  // S is read before the next cube's F1 overwrites P
   }
