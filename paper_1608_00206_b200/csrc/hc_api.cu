@@ -145,12 +145,12 @@ inline int& dev_slot(int* cache, int& scratch) {
 // ---- 8-axis tiles: single level (tile8_kernel) and two levels (prep + slab8_kernel) ----
 // persistent grid size for a T8 kernel: SMs x resident CTAs per SM
 template <class K>
-cudaError_t t8_grid(K kern, int& grid_max) {
+cudaError_t t8_grid(K kern, int& grid_max, size_t smem = T8Cfg<double>::SMEM) {
   if (grid_max) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T8Cfg<double>::SMEM);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int occ = 0, dev = 0, sms = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T8_NT, T8Cfg<double>::SMEM);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T8_NT, smem);
   if (e != cudaSuccess) return e;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -274,10 +274,11 @@ template <class T, int M, int EPI = 0, int P2CH = T8_P2CH>
 cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st,
                            bool prep) {
   auto kern = slab8_kernel<T, M, EPI, P2CH>;
+  constexpr size_t smem = T8Cfg<T, EPI >= 2 ? HC_NRAW_EPI : T8_NRAW>::SMEM;
   static int gm_cache[kMaxDev] = {};
   int gm_scratch = 0;
   int& grid_max = dev_slot(gm_cache, gm_scratch);
-  cudaError_t e = t8_grid(kern, grid_max);
+  cudaError_t e = t8_grid(kern, grid_max, smem);
   if (e != cudaSuccess) return e;
   const uint64_t items = (uint64_t)a.nslab * (upow3(M) + upow3(8) / (P2W * P2CH));
   const unsigned grid = (unsigned)(items < (uint64_t)grid_max ? items : (uint64_t)grid_max);
@@ -288,7 +289,7 @@ cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const Sla
     if (e != cudaSuccess) return e;
   }
   LaunchScope ls("slab", st);
-  kern<<<grid, T8_NT, T8Cfg<T>::SMEM, st>>>(xu, yu, z, a);
+  kern<<<grid, T8_NT, smem, st>>>(xu, yu, z, a);
   return cudaGetLastError();
 }
 

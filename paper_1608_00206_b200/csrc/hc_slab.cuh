@@ -101,12 +101,19 @@ constexpr int T8_SCHED = 224;         // scheduler / prefetch thread (warp 7: li
 // 128 elements (the b_a2 halves of the natural slice) per operand; the pads put the F1
 // lanes (op, b_a2, b_C) on 32 distinct 8-byte bank slots (RS_H2 = 8, RS_OP = 16 mod 32)
 constexpr int RS_H1 = 64, RS_H2 = 136, RS_OP = 304, RS_SZ = 608;
-// raw ring depth: the slices stream from HBM (the middle-axes tables) or L2; ~10 pairs of
-// lead (~3 us) hide the loaded-HBM latency across item boundaries
+// raw ring depth: the slices stream from HBM (the middle-axes tables) or L2.  Measured at
+// D = 20 (round 2): 1 stage 29.8 ms, 2 stages 26.9 ms, 3 27.4, 4 27.5, 5 27.7 -- two pairs of
+// lead already hide the load latency behind F2 and the tile work, and a shallower ring leaves
+// 9.7 KB more of the SM's shared memory / L1 to the rest (D = 16 int64: 0.342 -> 0.327 ms)
 #ifndef HC_NRAW
-#define HC_NRAW 4
+#define HC_NRAW 2
 #endif
 constexpr int T8_NRAW = HC_NRAW;
+// the fused-carry instantiations (EPI 2, 3) keep a 4-stage ring: with 2 their scheduler state
+// no longer fits the 128 registers (4 bytes of spills)
+#ifndef HC_NRAW_EPI
+#define HC_NRAW_EPI 4
+#endif
 // P stage (F1 output): op*PS_OP + b_a2*PS_A2 + e_S*PS_ROW + b_C, e_S = e_B + 27 e_a1.
 // PS_ROW = 10: the F2 lanes (consecutive e_S) read 16 B at a 80-B stride (conflict-free);
 // PS_A2 = 8 and PS_OP = 16 (mod 32): the F1 stores of one warp hit 32 distinct slots.
@@ -114,10 +121,10 @@ constexpr int PS_ROW = 10, PS_A2 = 840, PS_OP = 1680, PS_SZ = 3360;
 // tile exchange buffer S (3^8) and the pass-2 buffer alias the two P stages
 constexpr int T8_PBUF = 2 * PS_SZ + 8;
 
-template <class T>
+template <class T, int NR = T8_NRAW>
 struct T8Cfg {
   static constexpr int ALIAS = T8_PBUF > 6561 ? T8_PBUF : 6561;
-  static constexpr size_t SMEM = sizeof(T) * (size_t)(ALIAS + T8_NRAW * RS_SZ);
+  static constexpr size_t SMEM = sizeof(T) * (size_t)(ALIAS + NR * RS_SZ);
   static_assert(P2Cfg<6>::SIZE <= ALIAS && P2Cfg<5>::SIZE <= ALIAS, "pass-2 buffer aliases the P stages");
 };
 
@@ -172,15 +179,16 @@ __device__ __forceinline__ long long* ph_sh() {
 // and completes on its mbarrier.  `done` counts fills consumed by F1 (advanced identically
 // in every thread); `seq` (the scheduling thread T8_SCHED) counts fills issued.  Fill n may be issued once fill
 // n - T8_NRAW has been read, i.e. seq - done < T8_NRAW at a point after a barrier.
+template <int NR = T8_NRAW>
 struct RawRing {
-  uint64_t* bar;     // [T8_NRAW] in shared memory
+  uint64_t* bar;     // [NR] in shared memory
   uint32_t seq;      // fills issued so far (T8_SCHED)
   uint32_t done;     // fills consumed so far
 };
-template <class T>
-__device__ __forceinline__ void t8_issue(RawRing& rr, const T* sx, const T* sy, T* R, uint64_t pol) {
-  HC_ASSERT(rr.seq - rr.done < (uint32_t)T8_NRAW);  // never overwrite a stage F1 has not read
-  const uint32_t st = rr.seq % T8_NRAW;
+template <class T, int NR>
+__device__ __forceinline__ void t8_issue(RawRing<NR>& rr, const T* sx, const T* sy, T* R, uint64_t pol) {
+  HC_ASSERT(rr.seq - rr.done < (uint32_t)NR);  // never overwrite a stage F1 has not read
+  const uint32_t st = rr.seq % NR;
   uint64_t* bar = &rr.bar[st];
   T* dst = R + st * RS_SZ;
   mbar_arrive_tx(bar, 2 * 256 * sizeof(T));
@@ -190,9 +198,10 @@ __device__ __forceinline__ void t8_issue(RawRing& rr, const T* sx, const T* sy, 
   tma_load_1d(dst + RS_OP + RS_H2, sy + 128, 128 * sizeof(T), bar, pol);
   ++rr.seq;
 }
-__device__ __forceinline__ uint32_t t8_wait(RawRing& rr) {
-  const uint32_t st = rr.done % T8_NRAW;
-  mbar_wait(&rr.bar[st], (rr.done / T8_NRAW) & 1);
+template <int NR>
+__device__ __forceinline__ uint32_t t8_wait(RawRing<NR>& rr) {
+  const uint32_t st = rr.done % NR;
+  mbar_wait(&rr.bar[st], (rr.done / NR) & 1);
   ++rr.done;
   return st;
 }
@@ -266,10 +275,10 @@ struct Prefetch {
 
 // Fill the ring (T8_SCHED).  next(pf) advances the cursor to the next pass-1 item the CTA
 // will run (setting sx0, sy0, stride, base, freeb, s = 0, left) or returns false.
-template <class T, class Next>
-__device__ __forceinline__ void pf_pump(Prefetch& pf, RawRing& rr, T* R, uint64_t pol, Next&& next) {
+template <class T, int NR, class Next>
+__device__ __forceinline__ void pf_pump(Prefetch& pf, RawRing<NR>& rr, T* R, uint64_t pol, Next&& next) {
   bool fenced = false;
-  while (rr.seq - rr.done < (uint32_t)T8_NRAW) {
+  while (rr.seq - rr.done < (uint32_t)NR) {
     if (pf.left == 0 && !next(pf)) return;
     if (!fenced) {  // the stage's previous contents were read through the generic proxy
       fence_proxy_async();
@@ -286,11 +295,11 @@ __device__ __forceinline__ void pf_pump(Prefetch& pf, RawRing& rr, T* R, uint64_
 // One pass-1 tile with `npairs` top pairs whose raw slices arrive, in order, through the
 // ring (issued by the pump).  Computes the tile's 3^8 values (final for the single-level
 // engine, evaluation domain of the middle axes for the slab engine) and stores them to zt.
-template <class T, bool FINAL, class Pump, class Mid>
-__device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, RawRing& rr, uint64_t pol_out,
+template <class T, bool FINAL, int NR, class Pump, class Mid>
+__device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, RawRing<NR>& rr, uint64_t pol_out,
                                       Pump&& pump, Mid&& mid) {
   T* P = sm;                          // [2][PS_SZ]
-  T* R = sm + T8Cfg<T>::ALIAS;        // [T8_NRAW][RS_SZ]
+  T* R = sm + T8Cfg<T>::ALIAS;        // [NR][RS_SZ]
   T* S = sm;                          // [9][27][27] after the pair loop (aliases P)
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const bool unit = tid < 243;                     // F2 / inverse unit u = (e_a2, e_S)
@@ -365,9 +374,10 @@ __device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, Raw
   }
 }
 
+template <int NR = T8_NRAW>
 __device__ __forceinline__ void ring_init(uint64_t* bars) {
   if (threadIdx.x == T8_SCHED) {
-    for (int i = 0; i < T8_NRAW; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < NR; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -386,7 +396,7 @@ tile8_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z
   __shared__ __align__(8) uint64_t raw_bar[T8_NRAW];
   __shared__ Prefetch pf;
   ring_init(raw_bar);
-  RawRing rr{raw_bar, 0, 0};
+  RawRing<> rr{raw_bar, 0, 0};
   const int k = D - 8;
   // a single pair's slices are reused by many tiles (keep them in L2); a batch's are read once
   const uint64_t pol_in = nitems > nslab ? policy_evict_first() : policy_evict_last();
@@ -625,10 +635,11 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   __shared__ uint4 s_qm;  // {q of slots 0..2, -}: one load for the selection
   __shared__ uint4 s_jm;  // {j of slots 0..2, byte i of .w = slot i is a pass-1 item}
   __shared__ int s_sel;
-  __shared__ __align__(8) uint64_t raw_bar[T8_NRAW];
+  constexpr int NR = EPI >= 2 ? HC_NRAW_EPI : T8_NRAW;
+  __shared__ __align__(8) uint64_t raw_bar[NR];
   __shared__ Prefetch pf;
-  ring_init(raw_bar);
-  RawRing rr{raw_bar, 0, 0};
+  ring_init<NR>(raw_bar);
+  RawRing<NR> rr{raw_bar, 0, 0};
   const uint32_t ns = args.nslab;
   const uint32_t total = ns * (N1 + N2);
   const uint32_t lag = args.lag;

@@ -58,7 +58,7 @@ tile8n_kernel(const uint64_t* __restrict__ x, const uint64_t* __restrict__ y, ui
   __shared__ Prefetch pf;
   __shared__ uint32_t s_mag[2];  // max |x| and max |y| of the cube (saturated at 2^31)
   ring_init(raw_bar);
-  RawRing rr{raw_bar, 0, 0};
+  RawRing<> rr{raw_bar, 0, 0};
   const uint64_t pol_in = policy_evict_first();  // every cube's inputs are read once
   if (threadIdx.x == T8_SCHED) {
     pf.left = 0;
@@ -197,7 +197,7 @@ tile8_list_kernel(const uint64_t* __restrict__ x, const uint64_t* __restrict__ y
   __shared__ __align__(8) uint64_t raw_bar[T8_NRAW];
   __shared__ Prefetch pf;
   ring_init(raw_bar);
-  RawRing rr{raw_bar, 0, 0};
+  RawRing<> rr{raw_bar, 0, 0};
   const uint32_t n = *fb_count;
   const uint64_t pol_in = policy_evict_first();
   if (threadIdx.x == T8_SCHED) {
