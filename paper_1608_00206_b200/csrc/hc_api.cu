@@ -274,7 +274,7 @@ template <class T, int M, int EPI = 0, int P2CH = T8_P2CH>
 cudaError_t launch_slab8_m(const T* x, const T* y, T* z, T* xu, T* yu, const SlabArgs& a, cudaStream_t st,
                            bool prep) {
   auto kern = slab8_kernel<T, M, EPI, P2CH>;
-  constexpr size_t smem = T8Cfg<T, EPI >= 2 ? HC_NRAW_EPI : T8_NRAW>::SMEM;
+  constexpr size_t smem = T8Cfg<T, slab_nraw<M, EPI>()>::SMEM;
   static int gm_cache[kMaxDev] = {};
   int gm_scratch = 0;
   int& grid_max = dev_slot(gm_cache, gm_scratch);

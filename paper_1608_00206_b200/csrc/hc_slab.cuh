@@ -109,11 +109,14 @@ constexpr int RS_H1 = 64, RS_H2 = 136, RS_OP = 304, RS_SZ = 608;
 #define HC_NRAW 2
 #endif
 constexpr int T8_NRAW = HC_NRAW;
-// the fused-carry instantiations (EPI 2, 3) keep a 4-stage ring: with 2 their scheduler state
-// no longer fits the 128 registers (4 bytes of spills)
-#ifndef HC_NRAW_EPI
-#define HC_NRAW_EPI 4
+// the fused-carry instantiations with M = 5 (EPI 2, 3; conv1d at D = 13) keep a 4-stage ring:
+// with 2 their scheduler state no longer fits the 128 registers (4 bytes of spills); the M = 6
+// ones take 2 like the plain engine (f1 at D = 20: 39.06 -> 38.45 ms)
+#ifndef HC_NRAW_EPI5
+#define HC_NRAW_EPI5 4
 #endif
+template <int M, int EPI>
+__host__ __device__ constexpr int slab_nraw() { return EPI >= 2 && M == 5 ? HC_NRAW_EPI5 : T8_NRAW; }
 // P stage (F1 output): op*PS_OP + b_a2*PS_A2 + e_S*PS_ROW + b_C, e_S = e_B + 27 e_a1.
 // PS_ROW = 10: the F2 lanes (consecutive e_S) read 16 B at a 80-B stride (conflict-free);
 // PS_A2 = 8 and PS_OP = 16 (mod 32): the F1 stores of one warp hit 32 distinct slots.
@@ -635,7 +638,7 @@ slab8_kernel(const T* __restrict__ xu, const T* __restrict__ yu, T* __restrict__
   __shared__ uint4 s_qm;  // {q of slots 0..2, -}: one load for the selection
   __shared__ uint4 s_jm;  // {j of slots 0..2, byte i of .w = slot i is a pass-1 item}
   __shared__ int s_sel;
-  constexpr int NR = EPI >= 2 ? HC_NRAW_EPI : T8_NRAW;
+  constexpr int NR = slab_nraw<M, EPI>();
   __shared__ __align__(8) uint64_t raw_bar[NR];
   __shared__ Prefetch pf;
   ring_init<NR>(raw_bar);
