@@ -83,7 +83,7 @@ def _ep_worker(rank, world, port, D, k, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("D,k", [(8, 2), (9, 3)])
+@pytest.mark.parametrize("D,k", [(8, 2), (9, 3), (10, 5)])
 def test_two_rank_evalpoint_exchange(D, k):
     # the all-to-all of the evaluation-point variant (north_star (4)): after the exchange each
     # rank holds every point's values on exactly its own columns
