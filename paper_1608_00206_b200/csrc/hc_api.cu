@@ -508,7 +508,7 @@ struct hc_plan_s {
 // timed alone on a B200 (tools/shard_times.py, profiles/r02_shard_balance.txt);
 // HC_SHARD_ALPHA overrides it (calibration runs).
 static double shard_alpha() {
-  static const double a = getenv("HC_SHARD_ALPHA") ? atof(getenv("HC_SHARD_ALPHA")) : 13.0;
+  static const double a = getenv("HC_SHARD_ALPHA") ? atof(getenv("HC_SHARD_ALPHA")) : 11.0;
   return a;
 }
 static std::vector<uint64_t> compute_cuts(int k, int ngpu) {

@@ -56,7 +56,7 @@ def test_plan_without_device_fails_loudly(hc):
     assert ei.value.code == 5
 
 
-ALPHA = 13.0  # compute_cuts' fixed cost per slab, in pairs (fitted: profiles/r02_shard_balance.txt)
+ALPHA = 11.0  # compute_cuts' fixed cost per slab, in pairs (fitted: profiles/r02_shard_balance.txt)
 
 
 def _slab_cost(t, k):
