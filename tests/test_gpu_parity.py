@@ -380,7 +380,7 @@ def test_config_c5_d22_one_shard_of_eight(hc, orc):
 @pytest.mark.parametrize("D,k,dtype,nranks", [(11, 1, "int64", 2), (11, 2, "int64", 5), (12, 3, "int64", 3),
                                               (12, 4, "int64", 8), (10, 2, "float64", 4), (14, 4, "int64", 1),
                                               # D - k >= 13: the points run as one batch on the two-level engine
-                                              (15, 2, "int64", 2), (16, 2, "float64", 3), (17, 4, "int64", 8),
+                                              (15, 2, "int64", 2), (15, 2, "int64", 3), (16, 2, "float64", 3), (17, 4, "int64", 8),
                                               # k = 5: 243 points, interpolated in shared memory
                                               (9, 5, "int64", 8), (13, 5, "float64", 3), (17, 5, "int64", 7)])
 def test_evalpoint_variant_emulated_ranks(hc, orc, D, k, dtype, nranks):
