@@ -490,6 +490,7 @@ struct hc_plan_s {
   void* yu = nullptr;
   std::mutex order_mu;
   std::map<std::pair<uint64_t, uint64_t>, uint4*> orders;  // [u0,u1) -> device processing order
+  std::map<std::pair<uint64_t, uint64_t>, std::pair<uint2*, uint32_t>> pair_items;  // [u0,u1) -> (tile, pair) items
   // host entry point workspace
   void* dx = nullptr;
   void* dy = nullptr;
@@ -551,6 +552,19 @@ extern "C" hc_status hc_shard_range(int D, int ngpu, int rank, uint64_t* zb, uin
 }
 
 static const uint4* slab_order(hc_plan_t p, uint64_t u0, uint64_t u1);
+static std::pair<uint2*, uint32_t> pair_items(hc_plan_t p, uint64_t u0, uint64_t u1);
+
+// single-level int64 plans with fewer tiles than CTA slots run one item per (tile, pair) and
+// accumulate with atomics (tile8_pairs_kernel); HC_PAIR_SPLIT=0 turns it off.  Measured with the
+// L2 flushed (tools/r02/t25.py, per call incl. the zeroing): D = 10 / 11 / 12 11.1 / 11.3 / 15.3 us
+// against 12.3 / 16.4 / 24.4 us per tile; D = 9 (4 pairs) 11.2 against 10.2 us, so D >= 10 only
+static bool use_pair_split(const hc_plan_s* p) {
+  static const bool on = [] {
+    const char* s = getenv("HC_PAIR_SPLIT");
+    return !(s && s[0] == '0');
+  }();
+  return on && p->dtype == HC_INT64 && !p->g.two_level && p->D >= 10 && p->D <= 12;
+}
 
 extern "C" hc_status hc_plan_create(hc_plan_t* out, int D, hc_dtype dtype, int ngpu, int rank) {
   if (!out) return HC_ERR_NULL;
@@ -593,6 +607,10 @@ extern "C" hc_status hc_plan_create(hc_plan_t* out, int D, hc_dtype dtype, int n
       return HC_ERR_CAPACITY;
     }
   }
+  if (use_pair_split(p) && !pair_items(p, p->cuts[rank], p->cuts[rank + 1]).first) {
+    hc_plan_destroy(p);
+    return HC_ERR_CAPACITY;
+  }
   *out = p;
   return HC_OK;
 }
@@ -611,6 +629,7 @@ extern "C" hc_status hc_plan_destroy(hc_plan_t p) {
   cudaFree(p->app_b);
   cudaFree(p->app_mx);
   for (auto& kv : p->orders) cudaFree(kv.second);
+  for (auto& kv : p->pair_items) cudaFree(kv.second.first);
   for (auto& s : p->hs)
     if (s) cudaStreamDestroy(s);
   delete p;
@@ -668,6 +687,52 @@ static const uint4* slab_order(hc_plan_t p, uint64_t u0, uint64_t u1) {
   return d;
 }
 
+// (tile, pair) items of the tiles [u0, u1) for tile8_pairs_kernel: tile t - u0 and every subset
+// s of its free top bits (digit 1), in the prefetcher's ascending-subset order; cached per range
+static std::pair<uint2*, uint32_t> pair_items(hc_plan_t p, uint64_t u0, uint64_t u1) {
+  std::lock_guard<std::mutex> lk(p->order_mu);
+  auto key = std::make_pair(u0, u1);
+  auto it = p->pair_items.find(key);
+  if (it != p->pair_items.end()) return it->second;
+  std::vector<uint2> h;
+  for (uint64_t t = u0; t < u1; ++t) {
+    uint32_t freeb = 0;
+    uint64_t v = t;
+    for (int a = 0; a < p->g.k; ++a, v /= 3)
+      if (v % 3 == 1) freeb |= 1u << a;
+    uint32_t s = 0;
+    do {
+      h.push_back(make_uint2((uint32_t)(t - u0), s));
+      s = (s - freeb) & freeb;
+    } while (s != 0);
+  }
+  uint2* d = nullptr;
+  if (cudaMalloc(&d, sizeof(uint2) * h.size()) != cudaSuccess) {
+    cudaGetLastError();
+    return {nullptr, 0};
+  }
+  if (cudaMemcpy(d, h.data(), sizeof(uint2) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return {nullptr, 0};
+  }
+  return p->pair_items[key] = {d, (uint32_t)h.size()};
+}
+
+static cudaError_t launch_tile8_pairs(const uint64_t* x, const uint64_t* y, uint64_t* z, int D, uint64_t u0,
+                                      uint64_t nu, const uint2* items, uint32_t nitems, cudaStream_t st) {
+  static int gm_cache[kMaxDev] = {};
+  int gm_scratch = 0;
+  int& grid_max = dev_slot(gm_cache, gm_scratch);
+  cudaError_t e = t8_grid(tile8_pairs_kernel, grid_max);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(z, 0, sizeof(uint64_t) * nu * 6561ull, st);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)(nitems < (uint32_t)grid_max ? nitems : (uint32_t)grid_max);
+  LaunchScope ls("tile", st);
+  tile8_pairs_kernel<<<grid, T8_NT, T8Cfg<uint64_t>::SMEM, st>>>(x, y, z, D, u0, items, nitems);
+  return cudaGetLastError();
+}
+
 // units [u0, u1) of the plan's geometry into z (z points at unit u0)
 static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, uint64_t u0, uint64_t u1,
                            cudaStream_t st, int slot, unsigned long long* cout = nullptr, void* ring = nullptr,
@@ -677,7 +742,12 @@ static hc_status run_range(hc_plan_t p, const void* x, const void* y, void* z, u
   cudaError_t e;
   if (!g.two_level) {
     const int Ls = (p->D >= 9 && p->D <= 12) ? small_tile_axes(p->D) : 8;
-    if (Ls < 8) {
+    if (use_pair_split(p) && Ls == 8) {
+      const auto pi = pair_items(p, u0, u1);
+      if (!pi.first) return HC_ERR_CAPACITY;
+      e = launch_tile8_pairs((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)z, p->D, u0, u1 - u0, pi.first,
+                             pi.second, st);
+    } else if (Ls < 8) {
       if (p->dtype == HC_INT64)
         e = launch_tile_small<uint64_t>((const uint64_t*)x, (const uint64_t*)y, (uint64_t*)z, p->D, Ls, u0, u1 - u0, st);
       else

@@ -10,6 +10,7 @@
 // This file shares nothing with oracle/ (test infrastructure).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 // Bounds-checked development build (-DHC_CHECK, tools/build_variant.sh check -DHC_CHECK): logical

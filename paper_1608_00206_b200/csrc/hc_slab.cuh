@@ -298,9 +298,12 @@ __device__ __forceinline__ void pf_pump(Prefetch& pf, RawRing<NR>& rr, T* R, uin
 // One pass-1 tile with `npairs` top pairs whose raw slices arrive, in order, through the
 // ring (issued by the pump).  Computes the tile's 3^8 values (final for the single-level
 // engine, evaluation domain of the middle axes for the slab engine) and stores them to zt.
-template <class T, bool FINAL, int NR, class Pump, class Mid>
+// ATOMIC (uint64 only): the tile's values are added to z with 64-bit atomics instead of stored
+// (tile8_pairs_kernel: one pair's contribution per item)
+template <class T, bool FINAL, bool ATOMIC = false, int NR, class Pump, class Mid>
 __device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, RawRing<NR>& rr, uint64_t pol_out,
                                       Pump&& pump, Mid&& mid) {
+  static_assert(!ATOMIC || std::is_same<T, uint64_t>::value, "atomic accumulation is exact only in the wrapping uint64 ring");
   T* P = sm;                          // [2][PS_SZ]
   T* R = sm + T8Cfg<T>::ALIAS;        // [NR][RS_SZ]
   T* S = sm;                          // [9][27][27] after the pair loop (aliases P)
@@ -364,7 +367,8 @@ __device__ __forceinline__ void tile8(int npairs, T* __restrict__ zt, T* sm, Raw
       inv_reg<2, T>(v);
 #pragma unroll
       for (int e = 0; e < 9; ++e) {
-        if constexpr (FINAL) st_cs(zt + e * 729 + col, v[e]);
+        if constexpr (ATOMIC) atomicAdd(reinterpret_cast<unsigned long long*>(zt + e * 729 + col), (unsigned long long)v[e]);
+        else if constexpr (FINAL) st_cs(zt + e * 729 + col, v[e]);
         else st_hint(zt + e * 729 + col, v[e], pol_out);
       }
     }
@@ -432,6 +436,53 @@ tile8_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z
     HC_ASSERT(slab0 + (w - b * nslab) < upow3(k));
     trit_split(slab0 + (w - b * nslab), k, base, freeb);
     tile8<T, true>(1 << __popc(freeb), z + w * 6561ull, sm, rr, 0, pump, [] {});
+    __syncthreads();  // S (aliases P) is free before the next tile's F1
+  }
+}
+
+// Single-level int64 with few tiles (10 <= D <= 12: 3^(D-8) tiles for 148 x 2 CTA slots):
+// one item per (tile, direct-split pair) instead of per tile, so a tile's pairs run on
+// different SMs; each item interpolates its pair's contribution (the interpolation is linear)
+// and adds it to the tile with 64-bit atomics -- exact, since wrapping additions commute
+// (R3).  z is zeroed before the launch.  items[w] = {tile t of the launch, subset s
+// of the tile's free top bits} (PAPER.md 173-177: pair i_T = base | s, j_T = base | (free & ~s)).
+__global__ void __launch_bounds__(T8_NT, 2)
+tile8_pairs_kernel(const uint64_t* __restrict__ x, const uint64_t* __restrict__ y, uint64_t* __restrict__ z, int D,
+                   uint64_t slab0, const uint2* __restrict__ items, uint32_t nitems) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* sm = reinterpret_cast<uint64_t*>(smem_raw);
+  __shared__ __align__(8) uint64_t raw_bar[T8_NRAW];
+  __shared__ Prefetch pf;
+  ring_init(raw_bar);
+  RawRing<> rr{raw_bar, 0, 0};
+  const int k = D - 8;
+  const uint64_t pol_in = policy_evict_last();  // a slice is shared by the pairs of several tiles
+  if (threadIdx.x == T8_SCHED) {
+    pf.left = 0;
+    pf.pos = 0xffffffffu;
+  }
+  uint64_t* R = sm + T8Cfg<uint64_t>::ALIAS;
+  auto next = [&](Prefetch& c) -> bool {
+    const uint32_t np = c.pos + 1;
+    const uint64_t w = blockIdx.x + (uint64_t)np * gridDim.x;
+    if (w >= nitems) return false;
+    const uint2 it = items[w];
+    uint32_t base, freeb;
+    trit_split(slab0 + it.x, k, base, freeb);
+    HC_ASSERT((it.y & ~freeb) == 0);
+    c.pos = np;
+    c.sx0 = x;
+    c.sy0 = y;
+    c.stride = 256;
+    c.base = base;
+    c.freeb = freeb;
+    c.s = it.y;
+    c.left = 1;
+    return true;
+  };
+  auto pump = [&]() { pf_pump<uint64_t>(pf, rr, R, pol_in, next); };
+  for (uint64_t w = blockIdx.x; w < nitems; w += gridDim.x) {
+    tile8<uint64_t, true, true>(1, z + (uint64_t)items[w].x * 6561ull, sm, rr, 0, pump, [] {});
     __syncthreads();  // S (aliases P) is free before the next tile's F1
   }
 }
