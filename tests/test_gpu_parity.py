@@ -630,7 +630,7 @@ def test_slab_ring_lag_clamped():
 
 @pytest.mark.parametrize("env", [{"HC_SLAB_LAG": "2"}, {"HC_ENGINE": "slabx"}, {"HC_ENGINE": "slabx", "HC_SLABX_LAG": "1"},
                                  {"HC_P2_HEAD": "243"}, {"HC_KEEP_POLICY": "1", "HC_P2_PREFETCH": "1"},
-                                 {"HC_NARROW": "0"}])
+                                 {"HC_NARROW": "0"}, {"HC_PAIR_SPLIT": "0"}])
 def test_engine_variants_by_env(env):
     # engine knobs are environment variables read once per process: run them in a child
     # process against the oracle
