@@ -557,13 +557,15 @@ static std::pair<uint2*, uint32_t> pair_items(hc_plan_t p, uint64_t u0, uint64_t
 // single-level int64 plans with fewer tiles than CTA slots run one item per (tile, pair) and
 // accumulate with atomics (tile8_pairs_kernel); HC_PAIR_SPLIT=0 turns it off.  Measured with the
 // L2 flushed (tools/r02/t25.py, per call incl. the zeroing): D = 10 / 11 / 12 11.1 / 11.3 / 15.3 us
-// against 12.3 / 16.4 / 24.4 us per tile; D = 9 (4 pairs) 11.2 against 10.2 us, so D >= 10 only
+// against 12.3 / 16.4 / 24.4 us per tile; D = 9 (4 pairs) 11.2 against 10.2 us.  In a stream of
+// back-to-back calls the separate zeroing launch costs more than D = 10 gains (bench.py C1:
+// 18.9 against 17.9 us per step, kernel 10.1 against 12.8 us), so D >= 11 only
 static bool use_pair_split(const hc_plan_s* p) {
   static const bool on = [] {
     const char* s = getenv("HC_PAIR_SPLIT");
     return !(s && s[0] == '0');
   }();
-  return on && p->dtype == HC_INT64 && !p->g.two_level && p->D >= 10 && p->D <= 12;
+  return on && p->dtype == HC_INT64 && !p->g.two_level && p->D >= 11 && p->D <= 12;
 }
 
 extern "C" hc_status hc_plan_create(hc_plan_t* out, int D, hc_dtype dtype, int ngpu, int rank) {

@@ -440,7 +440,7 @@ tile8_kernel(const T* __restrict__ x, const T* __restrict__ y, T* __restrict__ z
   }
 }
 
-// Single-level int64 with few tiles (10 <= D <= 12: 3^(D-8) tiles for 148 x 2 CTA slots):
+// Single-level int64 with few tiles (D = 11, 12: 3^(D-8) tiles for 148 x 2 CTA slots):
 // one item per (tile, direct-split pair) instead of per tile, so a tile's pairs run on
 // different SMs; each item interpolates its pair's contribution (the interpolation is linear)
 // and adds it to the tile with 64-bit atomics -- exact, since wrapping additions commute
