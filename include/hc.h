@@ -92,7 +92,12 @@ hc_status hc_shard_info(hc_plan_t plan, int rank, uint64_t* z_begin, uint64_t* z
  * per slab) is balanced. */
 hc_status hc_shard_range(int D, int ngpu, int rank, uint64_t* z_begin, uint64_t* z_end);
 
-/* Whole convolution: x, y device pointers (2^D elements), z device pointer (3^D). */
+/* Whole convolution: x, y device pointers (2^D elements), z device pointer (3^D).
+ * Stream-ordered, no host synchronisation (the plan's processing order is uploaded at plan
+ * creation).  Results are deterministic: fp64 sums in a fixed order; int64 is exact mod 2^64
+ * (reading R3) -- at D = 11, 12 the engine zeroes z on the stream and adds each direct-split
+ * pair's contribution with 64-bit atomics, which commute exactly.  One call at a time per plan
+ * and stream slot (the plan's counters are reused). */
 hc_status hc_convolve(hc_plan_t plan, const void* x, const void* y, void* z, void* stream);
 
 /* This rank's share: x, y replicated (2^D each, device); z_shard has
