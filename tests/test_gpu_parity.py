@@ -239,7 +239,7 @@ def test_host_entry_point(hc, orc):
     _assert_close(zh.numpy(), orc.conv(x, y), x, y)
     # a shard of a 3-way split through the host entry point (chunked device output and
     # overlapped copies), int64 at D = 16 and D = 8 (single-level), = the device path
-    for D, n, r in ((16, 3, 1), (8, 1, 0), (10, 3, 2)):
+    for D, n, r in ((16, 3, 1), (8, 1, 0), (10, 3, 2), (12, 2, 1)):  # D = 12: the pair-split engine
         x, y = hcgen.make_pair(D, "int64", "uniform", 78 + D, -1000, 1000)
         p = hc.Plan(D, "int64", n, r)
         b, e = p.shard_info()
